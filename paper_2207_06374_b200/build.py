@@ -1,0 +1,80 @@
+"""Builds the in-tree CUDA library paper_2207_06374_b200/_lib/libtrstmi_b200.so.
+
+nvcc -gencode arch=compute_100a,code=sm_100a for every translation unit;
+-fmad=false so only the explicit fma() sites of the Canonical Arithmetic Spec
+fuse; host code with -ffp-contract=off for the same reason.
+Also builds the C++ host-API test binary when its sources exist.
+"""
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_build")
+LIBDIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(LIBDIR, "libtrstmi_b200.so")
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
+                 "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I", os.path.join(HERE, "..", "include")]
+
+INSTANCES = [(c, s) for c in (1, 0) for s in (32, 128, 256)]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed: %s\n%s\n%s" % (" ".join(cmd), r.stdout, r.stderr))
+    return r.stdout + r.stderr
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return False
+    t = os.path.getmtime(target)
+    return all(os.path.getmtime(d) <= t for d in deps)
+
+
+def sources():
+    out = []
+    for root, _, files in os.walk(CSRC):
+        for f in files:
+            if f.endswith((".cu", ".cuh", ".hpp", ".h", ".cpp")):
+                out.append(os.path.join(root, f))
+    out.append(os.path.join(HERE, "..", "include", "trstmi_b200.h"))
+    return out
+
+
+def build(verbose=False, force=False, jobs=None):
+    os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(LIBDIR, exist_ok=True)
+    deps = sources()
+    if not force and _newer(LIB, deps):
+        return LIB
+    jobs = jobs or max(2, min(8, os.cpu_count() or 2))
+    tasks = []
+    objs = []
+    for cplx, s in INSTANCES:
+        o = os.path.join(BUILD, "inst_%s_%d.o" % ("c" if cplx else "r", s))
+        objs.append(o)
+        tasks.append(COMMON + ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-c",
+                               os.path.join(CSRC, "instantiate.cu"), "-o", o])
+    o = os.path.join(BUILD, "trstmi_capi.o")
+    objs.append(o)
+    tasks.append(COMMON + ["-c", os.path.join(CSRC, "trstmi_capi.cu"), "-o", o])
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        for log in ex.map(lambda c: _run([NVCC] + c), tasks):
+            if verbose and log.strip():
+                print(log)
+    tmp = LIB + ".tmp"
+    _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"])
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

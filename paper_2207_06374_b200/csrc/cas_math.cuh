@@ -1,0 +1,85 @@
+// Canonical Arithmetic Spec (CAS) transcendentals on the device.
+//
+// The reference calls std::exp / std::log (smoothing.hpp:122,126).  glibc and
+// libdevice differ by an ulp on some inputs, and the FD Hessian-vector product
+// (smoothing.hpp:176-180) amplifies such differences ~1e5x, so decision parity
+// with the CPU oracle needs ONE exp/log definition on both sides.  These are
+// operation-for-operation the same as cas_exp / cas_log in the oracle
+// (oracle/cas_oracle.hpp); the file is compiled with -fmad=false so only the
+// explicit fma() sites fuse.  Accuracy vs correctly rounded: exp <= 0.85 ulp,
+// log <= 1.8 ulp (tests/test_oracle_math.py).
+#pragma once
+#include <cstdint>
+
+namespace trstmi_dev {
+
+__device__ __forceinline__ double pow2i(int k) {  // 2^k, -1022 <= k <= 1023
+  return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+}
+
+__device__ __forceinline__ double cas_exp(double x) {
+  if (!(x == x)) return x;
+  if (x > 709.782712893383973096) return __longlong_as_double(0x7ff0000000000000LL);
+  if (x < -745.2) return 0.0;
+  const double kd = rint(__dmul_rn(x, 1.4426950408889634));
+  double r = fma(-kd, 6.93147180369123816490e-01, x);
+  r = fma(-kd, 1.90821492927058770002e-10, r);
+  double p = 1.6059043836821613e-10;
+  p = fma(p, r, 2.08767569878680989792e-09);
+  p = fma(p, r, 2.50521083854417187751e-08);
+  p = fma(p, r, 2.75573192239858906526e-07);
+  p = fma(p, r, 2.75573192239858906526e-06);
+  p = fma(p, r, 2.48015873015873015873e-05);
+  p = fma(p, r, 1.98412698412698412698e-04);
+  p = fma(p, r, 1.38888888888888888889e-03);
+  p = fma(p, r, 8.33333333333333333333e-03);
+  p = fma(p, r, 4.16666666666666666667e-02);
+  p = fma(p, r, 1.66666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = static_cast<int>(kd);
+  if (k > 1000) return __dmul_rn(__dmul_rn(p, pow2i(k - 64)), 0x1.0p64);
+  if (k < -1000) return __dmul_rn(__dmul_rn(p, pow2i(k + 600)), 0x1.0p-600);
+  return __dmul_rn(p, pow2i(k));
+}
+
+__device__ __forceinline__ double cas_log(double x) {
+  if (!(x == x) || x < 0.0) return __longlong_as_double(0x7ff8000000000000LL);
+  if (x == 0.0) return __longlong_as_double(0xfff0000000000000LL);
+  if (x == __longlong_as_double(0x7ff0000000000000LL)) return x;
+  int e = 0;
+  if (x < 0x1.0p-1022) {
+    x = __dmul_rn(x, 0x1.0p54);
+    e = -54;
+  }
+  unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(x));
+  e += static_cast<int>((bits >> 52) & 0x7ff) - 1023;
+  bits = (bits & 0x000fffffffffffffULL) | 0x3ff0000000000000ULL;
+  double m = __longlong_as_double(static_cast<long long>(bits));
+  if (m > 1.4142135623730951) {
+    m = __dmul_rn(m, 0.5);
+    e += 1;
+  }
+  const double f = __dsub_rn(m, 1.0);
+  const double s = __ddiv_rn(f, __dadd_rn(2.0, f));
+  const double s2 = __dmul_rn(s, s);
+  double p = 1.0 / 25.0;
+  p = fma(p, s2, 1.0 / 23.0);
+  p = fma(p, s2, 1.0 / 21.0);
+  p = fma(p, s2, 1.0 / 19.0);
+  p = fma(p, s2, 1.0 / 17.0);
+  p = fma(p, s2, 1.0 / 15.0);
+  p = fma(p, s2, 1.0 / 13.0);
+  p = fma(p, s2, 1.0 / 11.0);
+  p = fma(p, s2, 1.0 / 9.0);
+  p = fma(p, s2, 1.0 / 7.0);
+  p = fma(p, s2, 1.0 / 5.0);
+  p = fma(p, s2, 1.0 / 3.0);
+  const double t = __dmul_rn(__dmul_rn(s, s2), p);
+  const double logm = __dadd_rn(__dmul_rn(2.0, s), __dmul_rn(2.0, t));
+  const double ed = static_cast<double>(e);
+  return fma(ed, 6.93147180369123816490e-01, fma(ed, 1.90821492927058770002e-10, logm));
+}
+
+}  // namespace trstmi_dev

@@ -1,0 +1,508 @@
+// C ABI (include/trstmi_b200.h) over the B200 kernels.  Host logic only:
+// argument validation with the reference's error semantics, device
+// workspaces, kernel-family dispatch, the rescue loop of the batched anneal
+// and the multistart best-of selection (solver.hpp:256-267).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/trstmi_b200.h"
+#include "batch_kernels.cuh"
+#include "host/host_common.hpp"
+#include "kernel_table.hpp"
+
+using namespace trstmi_dev;
+
+struct trstmi_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  int* counter = nullptr;
+  std::string err;
+};
+
+namespace {
+
+int fail(trstmi_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return fail((ctx), TRSTMI_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+Prob make_prob(int field, long long d, long long N) {
+  Prob P;
+  P.d = (int)d;
+  P.N = (int)N;
+  P.L = (field == TRSTMI_COMPLEX ? 2 : 1) * (int)d;
+  P.dim = P.L * P.N;
+  P.n = (int)(N * (N - 1) / 2);
+  return P;
+}
+
+int check_shape(trstmi_ctx* ctx, int field, long long d, long long N, const char* who) {
+  if (field != TRSTMI_COMPLEX && field != TRSTMI_REAL) return fail(ctx, TRSTMI_ERR_INVALID_ARG, std::string(who) + ": bad field");
+  if (d < 1) return fail(ctx, TRSTMI_ERR_INVALID_ARG, std::string(who) + ": need d >= 1");
+  if (N < 2) return fail(ctx, TRSTMI_ERR_INVALID_ARG, std::string(who) + ": need N >= 2");
+  if (d > 16 || N > 4096) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, std::string(who) + ": shape outside the small-frame kernel family (d <= 16)");
+  return TRSTMI_OK;
+}
+
+// Device buffer RAII for the host-pointer entry points.
+struct DBuf {
+  void* p = nullptr;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int trstmi_version(void) { return 1; }
+
+int trstmi_lanes(int field, int64_t d, int64_t N) {
+  const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
+  if (dim <= 64) return 32;
+  if (dim <= 256) return 128;
+  return 256;
+}
+
+void trstmi_cfg_defaults(trstmi_cfg* c, int field, int d, int N) {
+  std::memset(c, 0, sizeof(*c));
+  c->field = field;
+  c->d = d;
+  c->N = N;
+  c->n_stages = 0;
+  c->eps_target = 1e-7;
+  c->delta0 = 0.0;
+  c->delta_max = 1e3;
+  c->eta = 0.05;
+  c->shrink = 0.25;
+  c->grow = 2.0;
+  c->grad_tol = 1e-9;
+  c->max_outer = 200;
+  c->max_cg = 0;
+  c->cg_force_c = 0.5;
+  c->record_cap = 0;
+}
+
+double trstmi_welch_bound(int64_t d, int64_t N) { return trstmi_host::welch_bound(d, N); }
+
+int trstmi_default_schedule(int64_t N, double eps_target, double* out, int cap) {
+  try {
+    std::vector<double> s = trstmi_host::default_delta_schedule(N, eps_target);
+    for (int i = 0; i < (int)s.size() && i < cap; ++i) out[i] = s[i];
+    return (int)s.size();
+  } catch (...) {
+    return -1;
+  }
+}
+
+int trstmi_random_frames(int field, int64_t d, int64_t N, uint64_t seed, int64_t first, int64_t count, double* frames,
+                         uint64_t* rng_state) {
+  if (d < 1 || N < 1 || count < 0) return TRSTMI_ERR_INVALID_ARG;
+  const int64_t dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
+  for (int64_t t = 0; t < count; ++t) {
+    trstmi_host::SplitMix64 rng(trstmi_host::mix_seed(seed, (uint64_t)(first + t)));
+    trstmi_host::random_frame(field == TRSTMI_COMPLEX, d, N, rng, frames + t * dim);
+    if (rng_state) rng.save(rng_state + 3 * t);
+  }
+  return TRSTMI_OK;
+}
+
+int trstmi_ctx_create(int device, trstmi_ctx** out) {
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return TRSTMI_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= n) return TRSTMI_ERR_INVALID_ARG;
+  trstmi_ctx* ctx = new trstmi_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return TRSTMI_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&ctx->counter, 64 * sizeof(int)) != cudaSuccess) {
+    delete ctx;
+    return TRSTMI_ERR_CUDA;
+  }
+  *out = ctx;
+  return TRSTMI_OK;
+}
+
+int trstmi_ctx_destroy(trstmi_ctx* ctx) {
+  if (!ctx) return TRSTMI_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->counter) cudaFree(ctx->counter);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TRSTMI_OK;
+}
+
+const char* trstmi_last_error(const trstmi_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+// ------------------------------------------------------------------ eval / hvp / coherence
+static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t N, BatchArgs& A, cudaStream_t st) {
+  const int S = trstmi_lanes(field, d, N);
+  const KernelSet* ks = find_kernels(field == TRSTMI_COMPLEX, (int)d, S);
+  if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
+  const void* fn = kind == 0 ? ks->eval : kind == 1 ? ks->hvp : ks->coherence;
+  const long long dbl = kind == 2 ? (eval_smem_doubles(A.P, S) - 3LL * A.P.dim) : eval_smem_doubles(A.P, S);
+  const size_t bytes = (size_t)dbl * sizeof(double);
+  if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "frame too large for the small-frame kernels");
+  CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const long long grid = std::min<long long>(A.B, 65535LL);
+  if (grid <= 0) return TRSTMI_OK;
+  void* args[] = {&A};
+  CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(S), args, bytes, st));
+  CUDA_TRY(ctx, cudaGetLastError());
+  return TRSTMI_OK;
+}
+
+int trstmi_eval_batch_dev(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B, const double* pts,
+                          const double* delta, int squared, double* F, double* s, double* grad, double* weights,
+                          int64_t* zero_col, void* stream) {
+  if (!ctx) return TRSTMI_ERR_INVALID_ARG;
+  int rc = check_shape(ctx, field, d, N, "eval_objective");
+  if (rc) return rc;
+  BatchArgs A{};
+  A.P = make_prob(field, d, N);
+  A.B = B;
+  A.pts = pts;
+  A.delta = delta;
+  A.squared = squared;
+  A.F = F;
+  A.s = s;
+  A.out = grad;
+  A.weights = weights;
+  A.zero_col = reinterpret_cast<long long*>(zero_col);
+  cudaSetDevice(ctx->device);
+  return batch_launch(ctx, 0, field, d, N, A, stream ? (cudaStream_t)stream : ctx->stream);
+}
+
+int trstmi_eval_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B, const double* pts,
+                      const double* delta, int squared, double* F, double* s, double* grad, double* weights,
+                      int64_t* zero_col) {
+  if (!ctx) return TRSTMI_ERR_INVALID_ARG;
+  int rc = check_shape(ctx, field, d, N, "eval_objective");
+  if (rc) return rc;
+  for (int64_t b = 0; b < B; ++b)
+    if (!(delta[b] > 0.0)) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "eval_objective: delta <= 0");
+  cudaSetDevice(ctx->device);
+  const Prob P = make_prob(field, d, N);
+  const size_t vb = (size_t)B * P.dim * sizeof(double);
+  DBuf dp, dd, dF, ds, dg, dw, dz;
+  CUDA_TRY(ctx, cudaMalloc(&dp.p, vb));
+  CUDA_TRY(ctx, cudaMalloc(&dd.p, B * sizeof(double)));
+  CUDA_TRY(ctx, cudaMalloc(&dF.p, B * sizeof(double)));
+  CUDA_TRY(ctx, cudaMalloc(&ds.p, B * sizeof(double)));
+  CUDA_TRY(ctx, cudaMalloc(&dg.p, vb));
+  CUDA_TRY(ctx, cudaMalloc(&dz.p, B * sizeof(int64_t)));
+  if (weights) CUDA_TRY(ctx, cudaMalloc(&dw.p, (size_t)B * P.n * sizeof(double)));
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, pts, vb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, delta, B * sizeof(double), cudaMemcpyHostToDevice, st));
+  rc = trstmi_eval_batch_dev(ctx, field, d, N, B, (double*)dp.p, (double*)dd.p, squared, (double*)dF.p, (double*)ds.p,
+                             (double*)dg.p, (double*)dw.p, (int64_t*)dz.p, st);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(F, dF.p, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(s, ds.p, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(grad, dg.p, vb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(zero_col, dz.p, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (weights) CUDA_TRY(ctx, cudaMemcpyAsync(weights, dw.p, (size_t)B * P.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return TRSTMI_OK;
+}
+
+int trstmi_hvp_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B, const double* pts,
+                     const double* dirs, const double* delta, double* hv, int32_t* path, int64_t* zero_col) {
+  if (!ctx) return TRSTMI_ERR_INVALID_ARG;
+  int rc = check_shape(ctx, field, d, N, "hessian_vector_product");
+  if (rc) return rc;
+  for (int64_t b = 0; b < B; ++b)
+    if (!(delta[b] > 0.0)) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "eval_objective: delta <= 0");
+  cudaSetDevice(ctx->device);
+  const Prob P = make_prob(field, d, N);
+  const size_t vb = (size_t)B * P.dim * sizeof(double);
+  DBuf dp, dr, dd, dh, dpa, dz;
+  CUDA_TRY(ctx, cudaMalloc(&dp.p, vb));
+  CUDA_TRY(ctx, cudaMalloc(&dr.p, vb));
+  CUDA_TRY(ctx, cudaMalloc(&dd.p, B * sizeof(double)));
+  CUDA_TRY(ctx, cudaMalloc(&dh.p, vb));
+  CUDA_TRY(ctx, cudaMalloc(&dpa.p, B * sizeof(int32_t)));
+  CUDA_TRY(ctx, cudaMalloc(&dz.p, B * sizeof(int64_t)));
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, pts, vb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(dr.p, dirs, vb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, delta, B * sizeof(double), cudaMemcpyHostToDevice, st));
+  BatchArgs A{};
+  A.P = P;
+  A.B = B;
+  A.pts = (double*)dp.p;
+  A.dirs = (double*)dr.p;
+  A.delta = (double*)dd.p;
+  A.squared = 1;
+  A.out = (double*)dh.p;
+  A.path = (int*)dpa.p;
+  A.zero_col = (long long*)dz.p;
+  rc = batch_launch(ctx, 1, field, d, N, A, st);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(hv, dh.p, vb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(path, dpa.p, B * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(zero_col, dz.p, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return TRSTMI_OK;
+}
+
+int trstmi_coherence_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B, const double* frames,
+                           int normalize, double* mu, int64_t* argmax_pair, int64_t* zero_col) {
+  if (!ctx) return TRSTMI_ERR_INVALID_ARG;
+  int rc = check_shape(ctx, field, d, N, "coherence");
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  const Prob P = make_prob(field, d, N);
+  const size_t vb = (size_t)B * P.dim * sizeof(double);
+  DBuf dp, dm, da, dz;
+  CUDA_TRY(ctx, cudaMalloc(&dp.p, vb));
+  CUDA_TRY(ctx, cudaMalloc(&dm.p, B * sizeof(double)));
+  CUDA_TRY(ctx, cudaMalloc(&da.p, B * sizeof(int64_t)));
+  CUDA_TRY(ctx, cudaMalloc(&dz.p, B * sizeof(int64_t)));
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, frames, vb, cudaMemcpyHostToDevice, st));
+  BatchArgs A{};
+  A.P = P;
+  A.B = B;
+  A.pts = (double*)dp.p;
+  A.normalize = normalize;
+  A.mu = (double*)dm.p;
+  A.argmax = (long long*)da.p;
+  A.zero_col = (long long*)dz.p;
+  rc = batch_launch(ctx, 2, field, d, N, A, st);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(mu, dm.p, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(argmax_pair, da.p, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(zero_col, dz.p, B * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return TRSTMI_OK;
+}
+
+// ------------------------------------------------------------------ batched anneal
+static int resolve_cfg(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, std::vector<double>& sched) {
+  int rc = check_shape(ctx, c->field, c->d, c->N, "anneal");
+  if (rc) return rc;
+  A.P = make_prob(c->field, c->d, c->N);
+  if (c->n_stages < 0 || c->n_stages > TRSTMI_MAX_STAGES) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "anneal: bad n_stages");
+  if (c->n_stages == 0) {
+    try {
+      sched = trstmi_host::default_delta_schedule(c->N, c->eps_target);
+    } catch (const std::exception& e) {
+      return fail(ctx, TRSTMI_ERR_INVALID_ARG, e.what());
+    }
+  } else {
+    sched.assign(c->schedule, c->schedule + c->n_stages);
+  }
+  if ((int)sched.size() > TRSTMI_MAX_STAGES) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "anneal: schedule too long");
+  for (size_t k = 0; k + 1 < sched.size(); ++k)  // solver.hpp:172-176
+    if (!(sched[k] > sched[k + 1]) || sched[k + 1] <= 0.0)
+      return fail(ctx, TRSTMI_ERR_INVALID_ARG, "anneal: schedule must be strictly decreasing and positive");
+  if (!sched.empty() && !(sched[0] > 0.0)) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "eval_objective: delta <= 0");
+  A.n_stages = (int)sched.size();
+  for (int k = 0; k < A.n_stages; ++k) A.schedule[k] = sched[k];
+  TrCfg& t = A.tr;
+  const double dim = (double)A.P.dim;
+  t.delta0 = c->delta0 == 0.0 ? 0.1 * std::sqrt(dim) : c->delta0;  // trust_region.hpp:194-195
+  t.max_cg = c->max_cg == 0 ? (int)(2 * A.P.dim) : c->max_cg;
+  t.delta_max = c->delta_max;
+  t.eta = c->eta;
+  t.shrink = c->shrink;
+  t.grow = c->grow;
+  t.grad_tol = c->grad_tol;
+  t.cg_force_c = c->cg_force_c;
+  t.max_outer = c->max_outer;
+  if (!(t.delta0 > 0.0) || t.delta0 > t.delta_max)  // trust_region.hpp:196-204
+    return fail(ctx, TRSTMI_ERR_INVALID_ARG, "trust_region_minimize: need 0 < delta0 <= delta_max");
+  if (!(t.eta >= 0.0 && t.eta < 0.25)) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "trust_region_minimize: need 0 <= eta < 1/4");
+  if (!(t.shrink > 0.0 && t.shrink < 1.0 && t.grow > 1.0))
+    return fail(ctx, TRSTMI_ERR_INVALID_ARG, "trust_region_minimize: need 0 < shrink < 1 < grow");
+  A.record_cap = c->record_cap < 0 ? 0 : c->record_cap;
+  return TRSTMI_OK;
+}
+
+static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cudaStream_t st) {
+  const int S = trstmi_lanes(c->field, c->d, c->N);
+  const KernelSet* ks = find_kernels(c->field == TRSTMI_COMPLEX, c->d, S);
+  if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
+  const size_t bytes = (size_t)anneal_smem_doubles(A.P, S) * sizeof(double);
+  if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "trial state exceeds one SM's shared memory");
+  CUDA_TRY(ctx, cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  int per_sm = 0;
+  CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks->anneal, S, bytes));
+  if (per_sm < 1) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "anneal kernel cannot be resident");
+  const long long grid = std::min<long long>(A.n_list, (long long)per_sm * ctx->sm_count);
+  A.counter = ctx->counter;
+  CUDA_TRY(ctx, cudaMemsetAsync(ctx->counter, 0, sizeof(int), st));
+  if (grid <= 0) return TRSTMI_OK;
+  void* args[] = {&A};
+  CUDA_TRY(ctx, cudaLaunchKernel(ks->anneal, dim3((unsigned)grid), dim3(S), args, bytes, st));
+  CUDA_TRY(ctx, cudaGetLastError());
+  return TRSTMI_OK;
+}
+
+int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trials, double* params_dev,
+                           uint64_t* rng_state, double* frames_dev, trstmi_trial_out* trial_out_dev,
+                           trstmi_stage_out* stage_out_dev, trstmi_outer_out* outer_out_dev, void* stream) {
+  if (!ctx || !cfg) return TRSTMI_ERR_INVALID_ARG;
+  if (trials < 0 || trials > (1LL << 30)) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "bad trial count");
+  AnnealArgs A;
+  std::memset(&A, 0, sizeof(A));
+  std::vector<double> sched;
+  int rc = resolve_cfg(ctx, cfg, A, sched);
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  A.n_list = (int)trials;
+  A.params = params_dev;
+  A.frames = frames_dev;
+  A.tout = trial_out_dev;
+  A.sout = stage_out_dev;
+  A.oout = outer_out_dev;
+  rc = launch_anneal(ctx, cfg, A, st);
+  if (rc) return rc;
+  // Stage-boundary rescue loop (solver.hpp:139-156, 183): flagged trials get
+  // their collapsed columns redrawn from their own generator on the host and
+  // resume at the flagged stage.
+  std::vector<trstmi_trial_out> to((size_t)trials);
+  const bool cplx = cfg->field == TRSTMI_COMPLEX;
+  const int dim = A.P.dim;
+  for (int round = 0; trials > 0; ++round) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(to.data(), trial_out_dev, trials * sizeof(trstmi_trial_out), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    std::vector<int> list, start(trials, 0);
+    for (int64_t t = 0; t < trials; ++t) {
+      if (to[t].status != TRSTMI_TRIAL_NEED_RESCUE) continue;
+      std::vector<double> p(dim);
+      CUDA_TRY(ctx, cudaMemcpy(p.data(), params_dev + t * dim, dim * sizeof(double), cudaMemcpyDeviceToHost));
+      int bad;
+      if (rng_state) {
+        trstmi_host::SplitMix64 rng = trstmi_host::SplitMix64::load(rng_state + 3 * t);
+        bad = trstmi_host::rescue_zero_columns(cplx, cfg->d, cfg->N, p.data(), &rng);
+        rng.save(rng_state + 3 * t);
+      } else {
+        bad = trstmi_host::rescue_zero_columns(cplx, cfg->d, cfg->N, p.data(), nullptr);
+      }
+      if (bad >= 0) {  // ZeroColumnError escapes anneal: the restart fails
+        to[t].status = TRSTMI_TRIAL_ZERO_COLUMN;
+        to[t].zero_col = bad;
+        CUDA_TRY(ctx, cudaMemcpy(trial_out_dev + t, &to[t], sizeof(trstmi_trial_out), cudaMemcpyHostToDevice));
+        continue;
+      }
+      CUDA_TRY(ctx, cudaMemcpy(params_dev + t * dim, p.data(), dim * sizeof(double), cudaMemcpyHostToDevice));
+      list.push_back((int)t);
+      start[t] = to[t].fail_stage;
+    }
+    if (list.empty()) break;
+    if (round > 64 * A.n_stages) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "rescue loop did not converge");
+    DBuf dl, ds;
+    CUDA_TRY(ctx, cudaMalloc(&dl.p, list.size() * sizeof(int)));
+    CUDA_TRY(ctx, cudaMalloc(&ds.p, trials * sizeof(int)));
+    CUDA_TRY(ctx, cudaMemcpy(dl.p, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpy(ds.p, start.data(), trials * sizeof(int), cudaMemcpyHostToDevice));
+    A.list = (const int*)dl.p;
+    A.start_stage = (const int*)ds.p;
+    A.n_list = (int)list.size();
+    rc = launch_anneal(ctx, cfg, A, st);
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    A.list = nullptr;
+    A.start_stage = nullptr;
+  }
+  return TRSTMI_OK;
+}
+
+int trstmi_solve_batch(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trials, double* params, uint64_t* rng_state,
+                       double* frames, trstmi_trial_out* trial_out, trstmi_stage_out* stage_out,
+                       trstmi_outer_out* outer_out) {
+  if (!ctx || !cfg) return TRSTMI_ERR_INVALID_ARG;
+  AnnealArgs A;
+  std::memset(&A, 0, sizeof(A));
+  std::vector<double> sched;
+  int rc = resolve_cfg(ctx, cfg, A, sched);
+  if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  const size_t vb = (size_t)trials * A.P.dim * sizeof(double);
+  const size_t cap = (size_t)A.record_cap;
+  DBuf dp, df, dt, ds, dout;
+  CUDA_TRY(ctx, cudaMalloc(&dp.p, std::max<size_t>(vb, 8)));
+  if (frames) CUDA_TRY(ctx, cudaMalloc(&df.p, std::max<size_t>(vb, 8)));
+  CUDA_TRY(ctx, cudaMalloc(&dt.p, std::max<size_t>(trials * sizeof(trstmi_trial_out), 8)));
+  CUDA_TRY(ctx, cudaMalloc(&ds.p, std::max<size_t>(trials * A.n_stages * sizeof(trstmi_stage_out), 8)));
+  if (outer_out && cap) CUDA_TRY(ctx, cudaMalloc(&dout.p, trials * cap * sizeof(trstmi_outer_out)));
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, params, vb, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(ctx, cudaMemsetAsync(ds.p, 0, trials * A.n_stages * sizeof(trstmi_stage_out), st));
+  rc = trstmi_solve_batch_dev(ctx, cfg, trials, (double*)dp.p, rng_state, (double*)df.p, (trstmi_trial_out*)dt.p,
+                              (trstmi_stage_out*)ds.p, (trstmi_outer_out*)dout.p, st);
+  if (rc) return rc;
+  CUDA_TRY(ctx, cudaMemcpyAsync(params, dp.p, vb, cudaMemcpyDeviceToHost, st));
+  if (frames) CUDA_TRY(ctx, cudaMemcpyAsync(frames, df.p, vb, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaMemcpyAsync(trial_out, dt.p, trials * sizeof(trstmi_trial_out), cudaMemcpyDeviceToHost, st));
+  if (stage_out)
+    CUDA_TRY(ctx, cudaMemcpyAsync(stage_out, ds.p, trials * A.n_stages * sizeof(trstmi_stage_out), cudaMemcpyDeviceToHost, st));
+  if (outer_out && cap)
+    CUDA_TRY(ctx, cudaMemcpyAsync(outer_out, dout.p, trials * cap * sizeof(trstmi_outer_out), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return TRSTMI_OK;
+}
+
+int trstmi_solve(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restarts, uint64_t seed, int64_t first,
+                 double* best_frame, double* best_coherence, int64_t* best_restart, trstmi_trial_out* trial_out,
+                 trstmi_stage_out* stage_out) {
+  if (!ctx || !cfg) return TRSTMI_ERR_INVALID_ARG;
+  if (cfg->d < 1 || cfg->N < 1) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "solve: need d, N >= 1");
+  if (restarts < 1) return fail(ctx, TRSTMI_ERR_INVALID_ARG, "solve: need restarts >= 1");
+  const int64_t dim = (cfg->field == TRSTMI_COMPLEX ? 2 : 1) * (int64_t)cfg->d * cfg->N;
+  std::vector<double> params(restarts * dim), frames(restarts * dim);
+  std::vector<uint64_t> rng(restarts * 3);
+  int rc = trstmi_random_frames(cfg->field, cfg->d, cfg->N, seed, first, restarts, params.data(), rng.data());
+  if (rc) return fail(ctx, rc, "random_frame failed");
+  std::vector<trstmi_trial_out> to(restarts);
+  int n_stages = cfg->n_stages;
+  if (n_stages == 0) n_stages = std::max(0, trstmi_default_schedule(cfg->N, cfg->eps_target, nullptr, 0));
+  std::vector<trstmi_stage_out> so(restarts * std::max(n_stages, 1));
+  rc = trstmi_solve_batch(ctx, cfg, restarts, params.data(), rng.data(), frames.data(), to.data(), so.data(), nullptr);
+  if (rc) return rc;
+  int64_t best = -1;
+  double bc = 0.0;
+  for (int64_t i = 0; i < restarts; ++i) {  // solver.hpp:256-263
+    if (to[i].status != TRSTMI_TRIAL_OK) continue;
+    if (best < 0 || to[i].coherence < bc) {
+      best = i;
+      bc = to[i].coherence;
+    }
+  }
+  if (trial_out) std::memcpy(trial_out, to.data(), restarts * sizeof(trstmi_trial_out));
+  if (stage_out) std::memcpy(stage_out, so.data(), restarts * n_stages * sizeof(trstmi_stage_out));
+  if (best < 0) return fail(ctx, TRSTMI_ERR_ALL_FAILED, "solve: all restarts failed");
+  *best_restart = best;
+  *best_coherence = bc;
+  std::memcpy(best_frame, frames.data() + best * dim, dim * sizeof(double));
+  return TRSTMI_OK;
+}
+
+}  // extern "C"
