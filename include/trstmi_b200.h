@@ -147,6 +147,10 @@ int trstmi_ctx_create(int device, trstmi_ctx** out);
 int trstmi_ctx_destroy(trstmi_ctx* ctx);
 const char* trstmi_last_error(const trstmi_ctx* ctx);
 int trstmi_version(void);
+/* Number of kernels this library has launched (all contexts, all threads). */
+long long trstmi_launch_count(void);
+/* FP64 roofline denominator: measured DFMA throughput of the device (TFLOP/s). */
+int trstmi_measure_dfma_peak(trstmi_ctx* ctx, int iters, double* tflops);
 
 /* CAS reduction width S used for a shape: the lane count of
  * every dot / norm / z-sum.  The oracle takes the same S. */

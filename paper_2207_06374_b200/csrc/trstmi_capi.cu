@@ -19,6 +19,23 @@
 
 using namespace trstmi_dev;
 
+static long long g_launches = 0;  // kernels launched by this library (bench.py gpu_launches)
+
+// DFMA throughput probe (bench.py's FP64 roofline denominator): each thread
+// runs 8 independent fma chains.
+__global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (r == 12345.678) out[0] = r;
+}
+
 struct trstmi_ctx {
   int device = 0;
   int sm_count = 0;
@@ -71,6 +88,35 @@ struct DBuf {
 extern "C" {
 
 int trstmi_version(void) { return 1; }
+
+long long trstmi_launch_count(void) { return g_launches; }
+
+// Measured FP64 FMA peak of the device (TFLOP/s, 2 flops per fma), timed with
+// CUDA events over `iters` x 128 fma per thread on a full-occupancy grid.
+int trstmi_measure_dfma_peak(trstmi_ctx* ctx, int iters, double* tflops) {
+  if (!ctx) return TRSTMI_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  double* out = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&out, 8));
+  const int threads = 256;
+  const int blocks = ctx->sm_count * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(out, iters / 4 + 1, 0.999999, 1e-7);  // warm-up
+  cudaEventRecord(e0, ctx->stream);
+  dfma_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(out, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1, ctx->stream);
+  CUDA_TRY(ctx, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return TRSTMI_OK;
+}
 
 int trstmi_lanes(int field, int64_t d, int64_t N) {
   const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
@@ -172,6 +218,7 @@ static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t
   void* args[] = {&A};
   CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(S), args, bytes, st));
   CUDA_TRY(ctx, cudaGetLastError());
+  ++g_launches;
   return TRSTMI_OK;
 }
 
@@ -361,6 +408,7 @@ static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cu
   void* args[] = {&A};
   CUDA_TRY(ctx, cudaLaunchKernel(ks->anneal, dim3((unsigned)grid), dim3(S), args, bytes, st));
   CUDA_TRY(ctx, cudaGetLastError());
+  ++g_launches;
   return TRSTMI_OK;
 }
 
