@@ -41,15 +41,15 @@ struct AnnealArgs {
 };
 
 // doubles of shared memory the anneal kernel needs for a shape
-__host__ __device__ inline long long anneal_smem_doubles(const Prob& P, int S) {
+__host__ __device__ inline long long smem_doubles(const Prob& P, int S, bool cplx, int nvec) {
   const int W = S / 32;
-  return (long long)P.L * P.N + P.N + P.n + 2LL * 4 * W + 4 + 9LL * P.dim + W;  // +W: int scratch (2W ints)
+  return (long long)P.L * P.N + P.N + pair_smem_doubles(P, cplx) + 2LL * 4 * W + 4 + (long long)nvec * P.dim + W;
 }
-__host__ __device__ inline long long eval_smem_doubles(const Prob& P, int S) {
-  const int W = S / 32;
-  return (long long)P.L * P.N + P.N + P.n + 2LL * 4 * W + 4 + 3LL * P.dim + W;
+__host__ __device__ inline long long anneal_smem_doubles(const Prob& P, int S, bool cplx) {
+  return smem_doubles(P, S, cplx, 9);
 }
 
+template <bool CPLX>
 __device__ __forceinline__ void carve(const Prob& P, int S, double* base, Smem& sm, double** vecs, int nvec) {
   const int W = S / 32;
   double* p = base;
@@ -57,8 +57,12 @@ __device__ __forceinline__ void carve(const Prob& P, int S, double* base, Smem& 
   p += P.L * P.N;
   sm.alpha = p;
   p += P.N;
-  sm.cw = p;
+  sm.X = p;
   p += P.n;
+  sm.GR = p;
+  p += P.n;
+  sm.GI = p;
+  if (CPLX) p += P.n;
   sm.red = p;
   p += 2 * 4 * W;
   sm.scal = p;
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
   const int dim = P.dim;
   Smem sm;
   double* v[9];
-  carve(P, S, smem_raw, sm, v, 9);
+  carve<CPLX>(P, S, smem_raw, sm, v, 9);
   double* x = v[0];   // current iterate
   double* g = v[1];   // current gradient
   double* zs = v[2];  // Steihaug step z

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(S) eval_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[3];
-  carve(A.P, S, smem_raw, sm, v, 3);
+  carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
   int rbuf = 0;
   for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
     const double* x = A.pts + b * A.P.dim;
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(S) hvp_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[3];
-  carve(A.P, S, smem_raw, sm, v, 3);
+  carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
   double* gp = v[0];
   double* gm = v[1];
   double* g0 = v[2];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(S) coherence_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[1];
-  carve(A.P, S, smem_raw, sm, v, 0);
+  carve<CPLX>(A.P, S, smem_raw, sm, v, 0);
   int rbuf = 0;
   for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
     double mu = 0.0;

@@ -178,17 +178,80 @@ __device__ __forceinline__ void pair_advance(int N, int step, int& j, int& k) {
   }
 }
 
+// ------------------------------------------------------------------ division
+// Correctly rounded a/b from yb = RN(1/b) (Markstein's quotient correction:
+// q0 = RN(a*yb), r = a - b*q0 exact by fma, RN(q0 + r*yb) == RN(a/b) when
+// no intermediate under/overflows).  Bit-identical to IEEE division — the
+// oracle's '/' — and checked against __ddiv_rn in tests/test_gpu_parity.py.
+// Tiny numerators take the hardware division path.
+__device__ __forceinline__ double div_rn(double a, double b, double yb) {
+  if (fabs(a) < 0x1.0p-900) return __ddiv_rn(a, b);
+  const double q0 = __dmul_rn(a, yb);
+  const double r = fma(-q0, b, a);
+  return fma(r, yb, q0);
+}
+
 // ------------------------------------------------------------------ workspace
 // Shared-memory carve for one CTA.  phiS is component-major (phiS[q*N + j])
-// so consecutive pairs read consecutive columns without bank conflicts.
+// so a warp reading consecutive columns is bank-conflict free.  Per pair p:
+//   X[p]  : x_p (phase 2) -> w_p (phase 3) -> c_p*u_p, or -1 when c_p == 0
+//   GR[p] : Re G(j,k)     -> c_p * Re G(j,k)
+//   GI[p] : Im G(j,k)     -> c_p * Im G(j,k)      (complex frames only)
 struct Smem {
   double* phiS;   // L*N
   double* alpha;  // N
-  double* cw;     // n   (x_p, then w_p, then c_p = w_p / z)
+  double* X;      // n
+  double* GR;     // n
+  double* GI;     // n (complex) / 0 (real)
   double* red;    // 2 * 4 * W
   double* scal;   // 4 scalars (F of the last evaluation, ...)
   int* ired;      // 2 * W
 };
+
+__host__ __device__ inline long long pair_smem_doubles(const Prob& P, bool cplx) {
+  return (long long)P.n * (cplx ? 3 : 2);
+}
+
+// Gram of the upper triangle, row by row: warp w takes row pairs (a, N-2-a)
+// (N pairs per row pair), lanes walk k.  Calls f(p, re, im) per pair.
+template <bool CPLX, int DMAX, bool EXACT, int S, class F>
+__device__ __forceinline__ void gram_rows(const Prob& P, const double* __restrict__ phiS, F&& f) {
+  constexpr int W = S / 32;
+  const int d = EXACT ? DMAX : P.d;
+  const int N = P.N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nrp = N / 2;
+  for (int rp = warp; rp < nrp; rp += W) {
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+      const int j = side == 0 ? rp : N - 2 - rp;
+      if (side == 1 && j <= rp) break;
+      double a[(CPLX ? 2 : 1) * DMAX];
+#pragma unroll
+      for (int q = 0; q < (CPLX ? 2 : 1) * DMAX; ++q)
+        a[q] = (q < (CPLX ? 2 : 1) * d) ? phiS[q * N + j] : 0.0;
+      const int base = j * N - j * (j + 1) / 2 - j - 1;
+      for (int k = j + 1 + lane; k < N; k += 32) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int i = 0; i < DMAX; ++i) {
+          if (i < d) {
+            if constexpr (CPLX) {
+              const double br = phiS[(2 * i) * N + k], bi = phiS[(2 * i + 1) * N + k];
+              re = fma(a[2 * i], br, re);
+              re = fma(a[2 * i + 1], bi, re);
+              im = fma(a[2 * i], bi, im);
+              im = fma(-a[2 * i + 1], br, im);
+            } else {
+              re = fma(a[i], phiS[i * N + k], re);
+            }
+          }
+        }
+        f(base + k, re, im);
+      }
+    }
+  }
+}
 
 // ------------------------------------------------------------------ evaluation
 // eval_objective (smoothing.hpp:82-162) at p = x + sc*dir (sc == 0: p = x),
@@ -220,10 +283,14 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
     }
     const double a = sqrt(acc);
     sm.alpha[j] = a;
-    if (a < kZeroColumnTol) zc = min(zc, j);
+    if (a < kZeroColumnTol) {
+      zc = min(zc, j);
+    } else {
+      const double ya = __drcp_rn(a);
 #pragma unroll
-    for (int q = 0; q < C * DMAX; ++q)
-      if (q < C * d) sm.phiS[q * N + j] = __ddiv_rn(col[q], a);
+      for (int q = 0; q < C * DMAX; ++q)
+        if (q < C * d) sm.phiS[q * N + j] = div_rn(col[q], a, ya);
+    }
   }
   zc = block_min_int<S>(zc, sm.ired, rbuf);  // also publishes phiS / alpha
   if (zc != INT_MAX) {
@@ -236,119 +303,93 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
 
   // ---- phase 2: Gram upper triangle, x_p, s = max x_p (smoothing.hpp:104-118)
   double smax = -__longlong_as_double(0x7ff0000000000000LL);
-  if (tid < n) {
-    int j, k;
-    pair_first(N, tid, j, k);
-    for (int p = tid; p < n; p += S) {
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int i = 0; i < DMAX; ++i) {
-        if (i < d) {
-          if constexpr (CPLX) {
-            const double ar = sm.phiS[(2 * i) * N + j], ai = sm.phiS[(2 * i + 1) * N + j];
-            const double br = sm.phiS[(2 * i) * N + k], bi = sm.phiS[(2 * i + 1) * N + k];
-            re = fma(ar, br, re);
-            re = fma(ai, bi, re);
-            im = fma(ar, bi, im);
-            im = fma(-ai, br, im);
-          } else {
-            re = fma(sm.phiS[i * N + j], sm.phiS[i * N + k], re);
-          }
-        }
-      }
-      const double u = CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re);
-      const double xv = squared ? u : sqrt(u);
-      sm.cw[p] = xv;
-      smax = fmax(smax, xv);
-      pair_advance(N, S, j, k);
-    }
-  }
+  gram_rows<CPLX, DMAX, EXACT, S>(P, sm.phiS, [&](int p, double re, double im) {
+    const double u = CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re);
+    const double xv = squared ? u : sqrt(u);
+    sm.X[p] = xv;
+    sm.GR[p] = re;
+    if constexpr (CPLX) sm.GI[p] = im;
+    smax = fmax(smax, xv);
+  });
   const double s = block_max<S>(smax, sm.red, rbuf);
 
   // ---- phase 3: w_p = exp((x_p - s)/delta), z = CAS sum (smoothing.hpp:119-126)
   const double cut = __dmul_rn(kUnderflowCut, delta);
+  const double ydelta = __drcp_rn(delta);
   double zp = 0.0;
   for (int p = tid; p < n; p += S) {
-    const double diff = __dsub_rn(sm.cw[p], s);
-    const double w = (diff < cut) ? 0.0 : cas_exp(__ddiv_rn(diff, delta));
-    sm.cw[p] = w;
+    const double diff = __dsub_rn(sm.X[p], s);
+    double w = 0.0;
+    if (diff >= cut) w = cas_exp(div_rn(diff, delta, ydelta));
+    sm.X[p] = w;
     zp = __dadd_rn(zp, w);
   }
   const double z = block_sum1<S>(zp, sm.red, rbuf);
+  // ---- phase 3b: c_p = w_p / z and the pair coefficients of the gradient
+  // (smoothing.hpp:125, 136-142): c*u, c*Re G, c*Im G; c == 0 flagged -1.
+  const double yz = __drcp_rn(z);
   for (int p = tid; p < n; p += S) {
-    const double w = sm.cw[p];
-    const double c = (w == 0.0) ? 0.0 : __ddiv_rn(w, z);
-    sm.cw[p] = c;
+    const double w = sm.X[p];
+    const double c = (w == 0.0) ? 0.0 : div_rn(w, z, yz);
     if (wout) wout[p] = c;
+    if (c == 0.0) {
+      sm.X[p] = -1.0;
+    } else {
+      const double gr = sm.GR[p];
+      const double gi = CPLX ? sm.GI[p] : 0.0;
+      const double u = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+      double cc = c;
+      if (!squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(u), 1e-150)));
+      sm.X[p] = __dmul_rn(cc, u);
+      sm.GR[p] = __dmul_rn(cc, gr);
+      if constexpr (CPLX) sm.GI[p] = __dmul_rn(cc, gi);
+    }
   }
   if (F_out && tid == 0) *F_out = __dadd_rn(s, __dmul_rn(delta, cas_log(z)));
   if (s_out && tid == 0) *s_out = s;
   __syncthreads();
 
-  // ---- phase 4: gradient (smoothing.hpp:130-160), column m per thread,
-  // k ascending, pairs with c == 0 skipped; G(k,m) = conj(G(m,k)) for k > m.
-  for (int m = tid; m < N; m += S) {
-    double pm[C * DMAX], acc[C * DMAX];
-#pragma unroll
-    for (int q = 0; q < C * DMAX; ++q) {
-      acc[q] = 0.0;
-      pm[q] = (q < C * d) ? sm.phiS[q * N + m] : 0.0;
-    }
-    double t = 0.0;
-    int plo = m - 1;                         // p(k, m) for k = 0: m - 1
+  // ---- phase 4: gradient (smoothing.hpp:147-160).  One thread per output
+  // component (m, i): k ascending, pairs with c == 0 skipped, G(k,m) =
+  // conj(G(m,k)) for k > m.  t_m is recomputed by each of column m's threads.
+  for (int unit = tid; unit < N * d; unit += S) {
+    const int m = unit / d;
+    const int i = unit - m * d;
+    double acc_re = 0.0, acc_im = 0.0, t = 0.0;
+    int plo = m - 1;                                   // p(k, m) for k = 0
     const int prow = m * N - m * (m + 1) / 2 - m - 1;  // p(m, k) = prow + k
+    const double* pkr = sm.phiS + (C * i) * N;
+    const double* pki = sm.phiS + (C * i + 1) * N;
     for (int k = 0; k < N; ++k) {
       if (k == m) continue;
       const bool lower = k < m;
       const int p = lower ? plo : prow + k;
       if (lower) plo += N - k - 2;
-      double c = sm.cw[p];
-      if (c == 0.0) continue;
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int i = 0; i < DMAX; ++i) {
-        if (i < d) {
-          if constexpr (CPLX) {
-            const double kr = sm.phiS[(2 * i) * N + k], ki = sm.phiS[(2 * i + 1) * N + k];
-            const double mr = pm[2 * i], mi = pm[2 * i + 1];
-            // G(a,b) with a = min(k,m), b = max(k,m) (CAS gram_entry order)
-            const double ar = lower ? kr : mr, ai = lower ? ki : mi;
-            const double br = lower ? mr : kr, bi = lower ? mi : ki;
-            re = fma(ar, br, re);
-            re = fma(ai, bi, re);
-            im = fma(ar, bi, im);
-            im = fma(-ai, br, im);
-          } else {
-            re = fma(sm.phiS[i * N + k], pm[i], re);
-          }
-        }
-      }
-      const double Gr = re;
-      const double Gi = lower ? im : -im;  // G(k,m)
-      const double u = CPLX ? __dadd_rn(__dmul_rn(Gr, Gr), __dmul_rn(Gi, Gi)) : __dmul_rn(Gr, Gr);
-      if (!squared) c = __dmul_rn(c, __ddiv_rn(0.5, fmax(sqrt(u), 1e-150)));
-      t = __dadd_rn(t, __dmul_rn(c, u));
-      const double cr = __dmul_rn(c, Gr);
-      const double ci = __dmul_rn(c, Gi);
-#pragma unroll
-      for (int i = 0; i < DMAX; ++i) {
-        if (i < d) {
-          if constexpr (CPLX) {
-            const double pr = sm.phiS[(2 * i) * N + k], pi = sm.phiS[(2 * i + 1) * N + k];
-            acc[2 * i] = fma(pr, cr, acc[2 * i]);
-            acc[2 * i] = fma(-pi, ci, acc[2 * i]);
-            acc[2 * i + 1] = fma(pr, ci, acc[2 * i + 1]);
-            acc[2 * i + 1] = fma(pi, cr, acc[2 * i + 1]);
-          } else {
-            acc[i] = fma(sm.phiS[i * N + k], cr, acc[i]);
-          }
-        }
+      const double cu = sm.X[p];
+      if (cu < 0.0) continue;  // c == 0
+      t = __dadd_rn(t, cu);
+      const double cr = sm.GR[p];
+      const double pr = pkr[k];
+      if constexpr (CPLX) {
+        const double gi = sm.GI[p];
+        const double ci = lower ? gi : -gi;
+        const double pi = pki[k];
+        acc_re = fma(pr, cr, acc_re);
+        acc_re = fma(-pi, ci, acc_re);
+        acc_im = fma(pr, ci, acc_im);
+        acc_im = fma(pi, cr, acc_im);
+      } else {
+        acc_re = fma(pr, cr, acc_re);
       }
     }
     const double am = sm.alpha[m];
-#pragma unroll
-    for (int q = 0; q < C * DMAX; ++q)
-      if (q < C * d) gout[m * L + q] = __dmul_rn(__ddiv_rn(__dsub_rn(acc[q], __dmul_rn(t, pm[q])), am), 2.0);
+    const double ya = __drcp_rn(am);
+    const double pmr = sm.phiS[(C * i) * N + m];
+    gout[m * L + C * i] = __dmul_rn(div_rn(__dsub_rn(acc_re, __dmul_rn(t, pmr)), am, ya), 2.0);
+    if constexpr (CPLX) {
+      const double pmi = sm.phiS[(C * i + 1) * N + m];
+      gout[m * L + C * i + 1] = __dmul_rn(div_rn(__dsub_rn(acc_im, __dmul_rn(t, pmi)), am, ya), 2.0);
+    }
   }
   __syncthreads();
   return -1;
@@ -364,7 +405,7 @@ __device__ int coherence_cta(const Prob& P, const double* __restrict__ f, bool n
                              double* mu_out, long long* arg_out) {
   constexpr int C = CPLX ? 2 : 1;
   const int d = EXACT ? DMAX : P.d;
-  const int N = P.N, L = P.L, n = P.n;
+  const int N = P.N, L = P.L;
   const int tid = threadIdx.x;
   int zc = INT_MAX;
   for (int j = tid; j < N; j += S) {
@@ -378,42 +419,22 @@ __device__ int coherence_cta(const Prob& P, const double* __restrict__ f, bool n
       if (a < kZeroColumnTol) zc = min(zc, j);
     }
     sm.alpha[j] = a;
+    const double ya = __drcp_rn(a);
 #pragma unroll
     for (int q = 0; q < C * DMAX; ++q)
-      if (q < C * d) sm.phiS[q * N + j] = normalize ? __ddiv_rn(f[j * L + q], a) : f[j * L + q];
+      if (q < C * d) sm.phiS[q * N + j] = normalize ? div_rn(f[j * L + q], a, ya) : f[j * L + q];
   }
   zc = block_min_int<S>(zc, sm.ired, rbuf);
   if (zc != INT_MAX) return zc;
   double best = 0.0;
   long long arg = LLONG_MAX;
-  if (tid < n) {
-    int j, k;
-    pair_first(N, tid, j, k);
-    for (int p = tid; p < n; p += S) {
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int i = 0; i < DMAX; ++i) {
-        if (i < d) {
-          if constexpr (CPLX) {
-            const double ar = sm.phiS[(2 * i) * N + j], ai = sm.phiS[(2 * i + 1) * N + j];
-            const double br = sm.phiS[(2 * i) * N + k], bi = sm.phiS[(2 * i + 1) * N + k];
-            re = fma(ar, br, re);
-            re = fma(ai, bi, re);
-            im = fma(ar, bi, im);
-            im = fma(-ai, br, im);
-          } else {
-            re = fma(sm.phiS[i * N + j], sm.phiS[i * N + k], re);
-          }
-        }
-      }
-      const double m = sqrt(CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re));
-      if (m > best) {
-        best = m;
-        arg = p;
-      }
-      pair_advance(N, S, j, k);
+  gram_rows<CPLX, DMAX, EXACT, S>(P, sm.phiS, [&](int p, double re, double im) {
+    const double m = sqrt(CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re));
+    if (m > best || (m == best && m > 0.0 && p < arg)) {
+      best = m;
+      arg = p;
     }
-  }
+  });
   block_argmax<S>(best, arg, sm.red, rbuf);
   if (arg == LLONG_MAX) arg = -1;  // mu == 0 (or N < 2): no strict maximum above 0
   *mu_out = best;

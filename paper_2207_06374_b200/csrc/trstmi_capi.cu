@@ -36,6 +36,37 @@ __global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
   if (r == 12345.678) out[0] = r;
 }
 
+// Self-test kernels: device CAS transcendentals on caller data, and the
+// Markstein division against the hardware IEEE division on a seeded stream.
+__global__ void cas_math_kernel(const double* x, double* y, long long n, int which) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = which == 0 ? cas_exp(x[i]) : cas_log(x[i]);
+}
+
+__device__ __forceinline__ unsigned long long sm64(unsigned long long& s) {
+  unsigned long long z = (s += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void div_selftest_kernel(long long n, unsigned long long seed, unsigned long long* bad) {
+  unsigned long long s = seed ^ (0x632BE59BD9B4E019ULL * (blockIdx.x * (long long)blockDim.x + threadIdx.x + 1));
+  unsigned long long nb = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    // numerators: random significand, exponent in [-80, 20]; sign random;
+    // denominators: random significand, exponent in [-45, 15] (covers delta, z, alpha)
+    const unsigned long long r1 = sm64(s), r2 = sm64(s), r3 = sm64(s);
+    const double a = __longlong_as_double((long long)((r1 & 0x800fffffffffffffULL) |
+                                                      ((unsigned long long)(1023 - 80 + (r3 % 101)) << 52)));
+    const double b = __longlong_as_double((long long)((r2 & 0x000fffffffffffffULL) |
+                                                      ((unsigned long long)(1023 - 45 + ((r3 >> 20) % 61)) << 52)));
+    const double q = div_rn(a, b, __drcp_rn(b));
+    if (__double_as_longlong(q) != __double_as_longlong(__ddiv_rn(a, b))) ++nb;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 struct trstmi_ctx {
   int device = 0;
   int sm_count = 0;
@@ -118,9 +149,38 @@ int trstmi_measure_dfma_peak(trstmi_ctx* ctx, int iters, double* tflops) {
   return TRSTMI_OK;
 }
 
+int trstmi_selftest_cas_math(trstmi_ctx* ctx, int which, const double* x, double* y, int64_t n) {
+  if (!ctx || n < 0) return TRSTMI_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  DBuf dx, dy;
+  CUDA_TRY(ctx, cudaMalloc(&dx.p, std::max<int64_t>(n, 1) * 8));
+  CUDA_TRY(ctx, cudaMalloc(&dy.p, std::max<int64_t>(n, 1) * 8));
+  CUDA_TRY(ctx, cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
+  cas_math_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>((const double*)dx.p, (double*)dy.p, n, which);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpy(y, dy.p, n * 8, cudaMemcpyDeviceToHost));
+  return TRSTMI_OK;
+}
+
+int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t* mismatches) {
+  if (!ctx) return TRSTMI_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  DBuf db;
+  CUDA_TRY(ctx, cudaMalloc(&db.p, 8));
+  CUDA_TRY(ctx, cudaMemset(db.p, 0, 8));
+  div_selftest_kernel<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(n, seed, (unsigned long long*)db.p);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpy(mismatches, db.p, 8, cudaMemcpyDeviceToHost));
+  return TRSTMI_OK;
+}
+
 int trstmi_lanes(int field, int64_t d, int64_t N) {
   const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
+  const long long n = N * (N - 1) / 2;
   if (dim <= 64) return 32;
+  if (n >= 2048) return 512;
   if (dim <= 256) return 128;
   return 256;
 }
@@ -209,7 +269,7 @@ static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t
   const KernelSet* ks = find_kernels(field == TRSTMI_COMPLEX, (int)d, S);
   if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
   const void* fn = kind == 0 ? ks->eval : kind == 1 ? ks->hvp : ks->coherence;
-  const long long dbl = kind == 2 ? (eval_smem_doubles(A.P, S) - 3LL * A.P.dim) : eval_smem_doubles(A.P, S);
+  const long long dbl = smem_doubles(A.P, S, field == TRSTMI_COMPLEX, kind == 2 ? 0 : 3);
   const size_t bytes = (size_t)dbl * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "frame too large for the small-frame kernels");
   CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -395,7 +455,7 @@ static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cu
   const int S = trstmi_lanes(c->field, c->d, c->N);
   const KernelSet* ks = find_kernels(c->field == TRSTMI_COMPLEX, c->d, S);
   if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
-  const size_t bytes = (size_t)anneal_smem_doubles(A.P, S) * sizeof(double);
+  const size_t bytes = (size_t)anneal_smem_doubles(A.P, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "trial state exceeds one SM's shared memory");
   CUDA_TRY(ctx, cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   int per_sm = 0;

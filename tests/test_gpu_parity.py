@@ -194,3 +194,31 @@ def test_stage_boundary_rescue(ctx):
     assert np.array_equal(g["rng"], o["rng"])
     g2 = ctx.solve_batch(cfg, start[None], None)
     assert g2["trials"][0].status == abi.TRIAL_ZERO_COLUMN and g2["trials"][0].zero_col == 2
+
+
+def test_device_cas_math_bit_identical_to_oracle(ctx):
+    import ctypes
+    lib = ctx.lib
+    lib.trstmi_selftest_cas_math.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                             ctypes.c_int64]
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(-746, 710, 400000), rng.uniform(-50, 1, 400000), -(10 ** rng.uniform(-300, 3, 100000)),
+                        np.array([0.0, -0.0, -745.2, -745.13, 709.78, np.inf, -np.inf, np.nan])])
+    y = np.empty_like(x)
+    assert lib.trstmi_selftest_cas_math(ctx.h, 0, x.ctypes.data, y.ctypes.data, x.size) == 0
+    assert np.array_equal(y.view(np.uint64), orc.exp(x).view(np.uint64))
+    z = np.concatenate([rng.uniform(1, 5000, 400000), 10 ** rng.uniform(-300, 300, 400000), np.array([1.0, 2.0])])
+    w = np.empty_like(z)
+    assert lib.trstmi_selftest_cas_math(ctx.h, 1, z.ctypes.data, w.ctypes.data, z.size) == 0
+    assert np.array_equal(w.view(np.uint64), orc.log(z).view(np.uint64))
+
+
+def test_markstein_division_matches_ieee(ctx):
+    """The kernels divide by delta, z and alpha through a precomputed
+    reciprocal + one fma correction; it must equal IEEE division bit for bit."""
+    import ctypes
+    lib = ctx.lib
+    lib.trstmi_selftest_division.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p]
+    bad = ctypes.c_uint64()
+    assert lib.trstmi_selftest_division(ctx.h, 1 << 31, 20250809, ctypes.byref(bad)) == 0
+    assert bad.value == 0
