@@ -27,7 +27,8 @@
  * upper-triangular order: p(j,k) = j*N - j(j+1)/2 + (k-j-1)  (frame.hpp:80-91).
  *
  * Host pointers everywhere except the *_dev variants, which take device
- * pointers and a cudaStream_t passed as void*.
+ * pointers and a cudaStream_t passed as void* (used verbatim: NULL is the
+ * legacy default stream).
  */
 #ifndef TRSTMI_B200_H
 #define TRSTMI_B200_H
@@ -160,6 +161,8 @@ int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t
 /* CAS reduction width S used for a shape: the lane count of
  * every dot / norm / z-sum.  The oracle takes the same S. */
 int trstmi_lanes(int field, int64_t d, int64_t N);
+/* CAS gradient k-chunk count K for a shape. */
+int trstmi_kchunks(int field, int64_t d, int64_t N);
 /* Fills cfg with the reference defaults (trust_region.hpp:20-30, solver.hpp:21-29). */
 void trstmi_cfg_defaults(trstmi_cfg* cfg, int field, int d, int N);
 double trstmi_welch_bound(int64_t d, int64_t N);

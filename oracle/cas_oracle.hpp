@@ -174,14 +174,16 @@ inline double cas_log(double x) {
 }
 
 // ---------------------------------------------------------------- CAS sums
-// Lane-strided reduction of width S (a multiple of 32): lane l accumulates
-// elements l, l+S, l+2S, ... in ascending order starting from +0; each group
-// of 32 lanes is combined by an xor butterfly (offsets 16,8,4,2,1); the S/32
-// group results are added left to right.  This is the order a CTA of S
-// threads produces with __shfl_xor_sync + a sequential pass over warps.
+// Lane-strided reduction of width S (a power of two >= 32): lane l
+// accumulates elements l, l+S, l+2S, ... in ascending order starting from +0;
+// each group of 32 lanes is combined by an xor butterfly (offsets
+// 16,8,4,2,1); the S/32 group totals are then combined by the same butterfly
+// across groups (group offsets 1,2,4,...), i.e. a pairwise tree in group
+// order.  This is the order a CTA of S threads produces with
+// __shfl_xor_sync inside each warp and again across the warp totals.
 inline double butterfly_combine(std::vector<double>& lane, int S) {
   const int W = S / 32;
-  double total = 0.0;
+  std::vector<double> tot(W);
   for (int w = 0; w < W; ++w) {
     double a[32];
     for (int l = 0; l < 32; ++l) a[l] = lane[w * 32 + l];
@@ -190,9 +192,14 @@ inline double butterfly_combine(std::vector<double>& lane, int S) {
       for (int l = 0; l < 32; ++l) b[l] = a[l] + a[l ^ off];
       for (int l = 0; l < 32; ++l) a[l] = b[l];
     }
-    total = (w == 0) ? a[0] : total + a[0];
+    tot[w] = a[0];
   }
-  return total;
+  for (int off = 1; off < W; off <<= 1) {
+    std::vector<double> b(W);
+    for (int w = 0; w < W; ++w) b[w] = tot[w] + tot[w ^ off];
+    tot = b;
+  }
+  return tot[0];
 }
 
 inline double cas_sum(const double* v, std::int64_t n, int S) {
@@ -216,6 +223,7 @@ struct Shape {
   bool complex_field = true;  // false: real lines (new mode)
   std::int64_t d = 0, N = 0;
   int lanes = 32;             // CAS reduction width S (trstmi_lanes())
+  int kchunks = 1;            // CAS gradient k-chunks K (trstmi_kchunks())
   std::int64_t comps() const { return complex_field ? 2 : 1; }
   std::int64_t col_len() const { return comps() * d; }  // doubles per column
   std::int64_t dim() const { return col_len() * N; }
@@ -310,32 +318,46 @@ inline EvalResult eval_objective(const Shape& sh, const double* x, const double*
   // gradient (smoothing.hpp:130-160): per column m, k ascending, c == 0 skipped
   out.grad.assign(sh.dim(), 0.0);
   std::vector<double> acc(L);
+  // Gradient (smoothing.hpp:130-160) in the CAS order: for each column m the
+  // k-range is split into K = sh.kchunks contiguous chunks
+  // [c*N/K, (c+1)*N/K); inside a chunk t_m and the GEMM sums Phi * coeff
+  // (Eigen, smoothing.hpp:147) are ascending-k chains from +0 (t by add of
+  // c*u, the GEMM by fma); chunk partials are added left to right.
+  const int K = sh.kchunks;
+  std::vector<double> part(L);
   for (std::int64_t m = 0; m < N; ++m) {
     double t = 0.0;
     std::fill(acc.begin(), acc.end(), 0.0);
-    for (std::int64_t k = 0; k < N; ++k) {
-      if (k == m) continue;
-      const std::int64_t p = (k < m) ? pair_index(N, k, m) : pair_index(N, m, k);
-      double c = w[p];
-      if (c == 0.0) continue;
-      const double Gr = gre[p];
-      const double Gi = (k < m) ? gim[p] : -gim[p];  // G(k,m)
-      const double u = Gr * Gr + Gi * Gi;
-      if (!squared) c = c * (0.5 / std::max(std::sqrt(u), 1e-150));
-      t = t + c * u;
-      const double cr = c * Gr, ci = c * Gi;
-      const double* pk = &phi[k * L];
-      if (sh.complex_field) {
-        for (std::int64_t i = 0; i < sh.d; ++i) {
-          const double pr = pk[2 * i], pi = pk[2 * i + 1];
-          acc[2 * i] = std::fma(pr, cr, acc[2 * i]);
-          acc[2 * i] = std::fma(-pi, ci, acc[2 * i]);
-          acc[2 * i + 1] = std::fma(pr, ci, acc[2 * i + 1]);
-          acc[2 * i + 1] = std::fma(pi, cr, acc[2 * i + 1]);
+    for (int ch = 0; ch < K; ++ch) {
+      double tp = 0.0;
+      std::fill(part.begin(), part.end(), 0.0);
+      const std::int64_t k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
+      for (std::int64_t k = k_lo; k < k_hi; ++k) {
+        if (k == m) continue;
+        const std::int64_t p = (k < m) ? pair_index(N, k, m) : pair_index(N, m, k);
+        double c = w[p];
+        if (c == 0.0) continue;
+        const double Gr = gre[p];
+        const double Gi = (k < m) ? gim[p] : -gim[p];  // G(k,m)
+        const double u = Gr * Gr + Gi * Gi;
+        if (!squared) c = c * (0.5 / std::max(std::sqrt(u), 1e-150));
+        tp = tp + c * u;
+        const double cr = c * Gr, ci = c * Gi;
+        const double* pk = &phi[k * L];
+        if (sh.complex_field) {
+          for (std::int64_t i = 0; i < sh.d; ++i) {
+            const double pr = pk[2 * i], pi = pk[2 * i + 1];
+            part[2 * i] = std::fma(pr, cr, part[2 * i]);
+            part[2 * i] = std::fma(-pi, ci, part[2 * i]);
+            part[2 * i + 1] = std::fma(pr, ci, part[2 * i + 1]);
+            part[2 * i + 1] = std::fma(pi, cr, part[2 * i + 1]);
+          }
+        } else {
+          for (std::int64_t i = 0; i < sh.d; ++i) part[i] = std::fma(pk[i], cr, part[i]);
         }
-      } else {
-        for (std::int64_t i = 0; i < sh.d; ++i) acc[i] = std::fma(pk[i], cr, acc[i]);
       }
+      t = (ch == 0) ? tp : t + tp;
+      for (std::int64_t q = 0; q < L; ++q) acc[q] = (ch == 0) ? part[q] : acc[q] + part[q];
     }
     const double* pm = &phi[m * L];
     for (std::int64_t q = 0; q < L; ++q) out.grad[m * L + q] = ((acc[q] - t * pm[q]) / alpha[m]) * 2.0;

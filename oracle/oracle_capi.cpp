@@ -12,12 +12,22 @@ using namespace orc;
 
 namespace {
 
+// CAS shape parameters: the oracle takes the lane count S from
+// the caller and derives the gradient chunk count K from (N, d, S) by the
+// same rule as trstmi_kchunks().
+int kchunks_for(std::int64_t d, std::int64_t N, int S) {
+  (void)d;
+  const std::int64_t K = S / N;
+  return (int)(K < 1 ? 1 : (K > 8 ? 8 : K));
+}
+
 Shape make_shape(int field, std::int64_t d, std::int64_t N, int lanes) {
   Shape sh;
   sh.complex_field = (field == TRSTMI_COMPLEX);
   sh.d = d;
   sh.N = N;
   sh.lanes = lanes;
+  sh.kchunks = kchunks_for(d, N, lanes);
   return sh;
 }
 
@@ -126,6 +136,7 @@ void run_trial(const SolverConfig& cfg, const trstmi_cfg* c, std::int64_t t, dou
 
 extern "C" {
 
+int orc_kchunks(std::int64_t d, std::int64_t N, int S) { return kchunks_for(d, N, S); }
 double orc_exp(double x) { return cas_exp(x); }
 double orc_log(double x) { return cas_log(x); }
 void orc_exp_array(const double* x, double* y, std::int64_t n) {

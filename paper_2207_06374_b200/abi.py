@@ -84,8 +84,6 @@ def lanes_for(field, d, N):
     dim = dim_of(field, d, N)
     if dim <= 64:
         return 32
-    if N * (N - 1) // 2 >= 2048:
-        return 512
     if dim <= 256:
         return 128
     return 256

@@ -22,7 +22,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
                  "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I", os.path.join(HERE, "..", "include")]
 
-INSTANCES = [(c, s) for c in (1, 0) for s in (32, 128, 256, 512)]
+INSTANCES = [(c, s) for c in (1, 0) for s in (32, 128, 256)]
 
 
 def _run(cmd):

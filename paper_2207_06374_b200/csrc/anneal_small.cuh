@@ -43,7 +43,7 @@ struct AnnealArgs {
 // doubles of shared memory the anneal kernel needs for a shape
 __host__ __device__ inline long long smem_doubles(const Prob& P, int S, bool cplx, int nvec) {
   const int W = S / 32;
-  return (long long)P.L * P.N + P.N + pair_smem_doubles(P, cplx) + 2LL * 4 * W + 4 + (long long)nvec * P.dim + W;
+  return (long long)P.L * P.N + P.N + pair_smem_doubles(P, cplx) + 1 + 2LL * 4 * W + 4 + (long long)nvec * P.dim + W;
 }
 __host__ __device__ inline long long anneal_smem_doubles(const Prob& P, int S, bool cplx) {
   return smem_doubles(P, S, cplx, 9);
@@ -57,12 +57,14 @@ __device__ __forceinline__ void carve(const Prob& P, int S, double* base, Smem& 
   p += P.L * P.N;
   sm.alpha = p;
   p += P.N;
-  sm.X = p;
+  sm.U = p;
   p += P.n;
-  sm.GR = p;
-  p += P.n;
-  sm.GI = p;
-  if (CPLX) p += P.n;
+  sm.part = p;
+  p += (long long)P.K * P.N * (P.L + 1);
+  sm.mask = reinterpret_cast<unsigned*>(p);
+  p += ((long long)P.N * mask_words(P.N) + 1) / 2;
+  sm.jk = reinterpret_cast<unsigned*>(p);
+  p += ((long long)P.n + 1) / 2;
   sm.red = p;
   p += 2 * 4 * W;
   sm.scal = p;
@@ -88,7 +90,7 @@ __device__ __forceinline__ int all_finite(const double* v, int n, const Smem& sm
 }
 
 template <bool CPLX, int DMAX, bool EXACT, int S>
-__global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
+__global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kernel(const AnnealArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   const Prob P = A.P;
   const int tid = threadIdx.x;
@@ -96,6 +98,7 @@ __global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
   Smem sm;
   double* v[9];
   carve<CPLX>(P, S, smem_raw, sm, v, 9);
+  build_pair_table<S>(P, sm.jk);
   double* x = v[0];   // current iterate
   double* g = v[1];   // current gradient
   double* zs = v[2];  // Steihaug step z
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
       // ---- x0 evaluation (trust_region.hpp:206-209)
       double Fcur;
       ++evals;
-      const int zc0 = eval_cta<CPLX, DMAX, EXACT, S>(P, x, nullptr, 0.0, delta, true, sm, rbuf, g, &sm.scal[0], nullptr, nullptr);
+      const int zc0 = eval_cta<CPLX, DMAX, EXACT, S>(P, x, nullptr, 0.0, delta, sm, rbuf, g, &sm.scal[0], nullptr, nullptr);
       Fcur = sm.scal[0];
       (void)zc0;
       {
@@ -206,9 +209,9 @@ __global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
               const double h = kFdBaseStep * (1.0 + xnorm) / fmax(dn, 1e-300);
               __syncthreads();
               evals += 2;
-              const int zp = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, h, delta, true, sm, rbuf, bd, nullptr, nullptr, nullptr);
+              const int zp = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, h, delta, sm, rbuf, bd, nullptr, nullptr, nullptr);
               if (zp < 0) {
-                const int zm = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, -h, delta, true, sm, rbuf, gt, nullptr, nullptr, nullptr);
+                const int zm = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
                 if (zm < 0) {
                   const double h2 = 2.0 * h;
                   for (int i = tid; i < dim; i += S) bd[i] = (bd[i] - gt[i]) / h2;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
                 }
               } else {  // x+hd hit a zero column: g0, retry forward (fails again), backward
                 evals += 2;
-                const int zm = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, -h, delta, true, sm, rbuf, gt, nullptr, nullptr, nullptr);
+                const int zm = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
                 if (zm >= 0) {
                   status = TRSTMI_TRIAL_ZERO_COLUMN;
                   zero_col = zm;
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(S) anneal_small_kernel(const AnnealArgs A) {
           __syncthreads();
           ++evals;
           double Ft;
-          eval_cta<CPLX, DMAX, EXACT, S>(P, xt, nullptr, 0.0, delta, true, sm, rbuf, gt, &sm.scal[0], nullptr, nullptr);
+          eval_cta<CPLX, DMAX, EXACT, S>(P, xt, nullptr, 0.0, delta, sm, rbuf, gt, &sm.scal[0], nullptr, nullptr);
           Ft = sm.scal[0];
           const int gfin = all_finite<S>(gt, dim, sm, rbuf);
           const bool finite = isfinite(Ft) && gfin;

@@ -27,18 +27,22 @@ struct BatchArgs {
 };
 
 template <bool CPLX, int DMAX, bool EXACT, int S>
-__global__ void __launch_bounds__(S) eval_batch_kernel(const BatchArgs A) {
+__global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) eval_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[3];
   carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
+  build_pair_table<S>(A.P, sm.jk);
   int rbuf = 0;
   for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
     const double* x = A.pts + b * A.P.dim;
     double F, s;
-    const int zc = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, A.delta[b], A.squared != 0, sm, rbuf,
-                                                  A.out + b * A.P.dim, &sm.scal[0], &sm.scal[1],
-                                                  A.weights ? A.weights + b * A.P.n : nullptr);
+    double* wo = A.weights ? A.weights + b * A.P.n : nullptr;
+    const int zc = A.squared
+                       ? eval_cta<CPLX, DMAX, EXACT, S, true>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf,
+                                                              A.out + b * A.P.dim, &sm.scal[0], &sm.scal[1], wo)
+                       : eval_cta<CPLX, DMAX, EXACT, S, false>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf,
+                                                               A.out + b * A.P.dim, &sm.scal[0], &sm.scal[1], wo);
     F = sm.scal[0];
     s = sm.scal[1];
     if (threadIdx.x == 0) {
@@ -53,11 +57,12 @@ __global__ void __launch_bounds__(S) eval_batch_kernel(const BatchArgs A) {
 // make_hvp_factory(obj)(x)(dir) (solver.hpp:118-137) around
 // fd_hessian_vector_product (smoothing.hpp:167-181).
 template <bool CPLX, int DMAX, bool EXACT, int S>
-__global__ void __launch_bounds__(S) hvp_batch_kernel(const BatchArgs A) {
+__global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) hvp_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[3];
   carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
+  build_pair_table<S>(A.P, sm.jk);
   double* gp = v[0];
   double* gm = v[1];
   double* g0 = v[2];
@@ -77,21 +82,21 @@ __global__ void __launch_bounds__(S) hvp_batch_kernel(const BatchArgs A) {
       path = TRSTMI_HVP_ZERO_DIR;
     } else {
       const double h = kFdBaseStep * (1.0 + sqrt(nn[1])) / fmax(dn, 1e-300);
-      const int zp = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, h, delta, true, sm, rbuf, gp, nullptr, nullptr, nullptr);
+      const int zp = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, h, delta, sm, rbuf, gp, nullptr, nullptr, nullptr);
       if (zp < 0) {
-        const int zm = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, -h, delta, true, sm, rbuf, gm, nullptr, nullptr, nullptr);
+        const int zm = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
         if (zm < 0) {
           const double h2 = 2.0 * h;
           for (int i = threadIdx.x; i < dim; i += S) hv[i] = (gp[i] - gm[i]) / h2;
           path = TRSTMI_HVP_CENTRAL;
         } else {
-          eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, delta, true, sm, rbuf, g0, nullptr, nullptr, nullptr);
+          eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, delta, sm, rbuf, g0, nullptr, nullptr, nullptr);
           for (int i = threadIdx.x; i < dim; i += S) hv[i] = (gp[i] - g0[i]) / h;
           path = TRSTMI_HVP_FORWARD;
         }
       } else {
-        eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, delta, true, sm, rbuf, g0, nullptr, nullptr, nullptr);
-        const int zm = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, -h, delta, true, sm, rbuf, gm, nullptr, nullptr, nullptr);
+        eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, delta, sm, rbuf, g0, nullptr, nullptr, nullptr);
+        const int zm = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
         if (zm < 0) {
           for (int i = threadIdx.x; i < dim; i += S) hv[i] = (g0[i] - gm[i]) / h;
           path = TRSTMI_HVP_BACKWARD;
@@ -111,11 +116,12 @@ __global__ void __launch_bounds__(S) hvp_batch_kernel(const BatchArgs A) {
 }
 
 template <bool CPLX, int DMAX, bool EXACT, int S>
-__global__ void __launch_bounds__(S) coherence_batch_kernel(const BatchArgs A) {
+__global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) coherence_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[1];
   carve<CPLX>(A.P, S, smem_raw, sm, v, 0);
+  build_pair_table<S>(A.P, sm.jk);
   int rbuf = 0;
   for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
     double mu = 0.0;

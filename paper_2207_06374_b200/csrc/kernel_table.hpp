@@ -13,23 +13,19 @@ struct KernelSet {
 const KernelSet* trstmi_kernels_c_32(int d);
 const KernelSet* trstmi_kernels_c_128(int d);
 const KernelSet* trstmi_kernels_c_256(int d);
-const KernelSet* trstmi_kernels_c_512(int d);
 const KernelSet* trstmi_kernels_r_32(int d);
 const KernelSet* trstmi_kernels_r_128(int d);
 const KernelSet* trstmi_kernels_r_256(int d);
-const KernelSet* trstmi_kernels_r_512(int d);
 
 inline const KernelSet* find_kernels(bool cplx, int d, int S) {
   if (cplx) {
     if (S == 32) return trstmi_kernels_c_32(d);
     if (S == 128) return trstmi_kernels_c_128(d);
     if (S == 256) return trstmi_kernels_c_256(d);
-    if (S == 512) return trstmi_kernels_c_512(d);
   } else {
     if (S == 32) return trstmi_kernels_r_32(d);
     if (S == 128) return trstmi_kernels_r_128(d);
     if (S == 256) return trstmi_kernels_r_256(d);
-    if (S == 512) return trstmi_kernels_r_512(d);
   }
   return nullptr;
 }

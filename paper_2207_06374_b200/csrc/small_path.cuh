@@ -6,15 +6,10 @@
 // Every floating-point operation follows the Canonical Arithmetic Spec
 // so results are bit-identical to the CPU oracle: the file is
 // compiled with -fmad=false and fuses only at explicit fma() sites; all CTA
-// reductions use the CAS lane-strided / xor-butterfly / warp-sequential order.
+// reductions use the CAS lane-strided / xor-butterfly order.
 //
 // Reference functions restated here (paths under /root/reference/proj/include/trstmi):
 //   eval_cta            eval_objective           smoothing.hpp:82-162
-//   hvp (in tr loop)    make_hvp_factory         solver.hpp:118-137
-//                       fd_hessian_vector_product smoothing.hpp:167-181
-//   steihaug (inline)   steihaug_cg              trust_region.hpp:81-154
-//   tr loop             trust_region_minimize    trust_region.hpp:189-295
-//   stage loop          anneal                   solver.hpp:164-204
 //   coherence_cta       coherence/normalize      frame.hpp:60-69,138-145
 #pragma once
 #include <climits>
@@ -30,15 +25,57 @@ constexpr double kFdBaseStep = 0x1.965fea53d6e3dp-18;  // smoothing.hpp:16-17 (g
 constexpr double kUnderflowCut = -746.0;               // exp((x-s)/delta) == 0 below this * delta
 constexpr unsigned FULL = 0xffffffffu;
 
-struct Prob {
-  int d, N, L, dim, n;  // L = doubles per column (2d complex, d real); n = pairs
+#ifdef TRSTMI_PHASE_TIMERS
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_MARK(i)                                                        \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      const long long now_ = clock64();                                      \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(now_ - t_phase_)); \
+      t_phase_ = now_;                                                       \
+    }                                                                        \
+  } while (0)
+#define PHASE_START long long t_phase_ = clock64()
+#else
+#define PHASE_MARK(i) \
+  do {                \
+  } while (0)
+#define PHASE_START
+#endif
+
+template <bool B>
+struct BoolTag {
+  static constexpr bool value = B;
 };
 
+struct Prob {
+  int d, N, L, dim, n;  // L = doubles per column (2d complex, d real); n = pairs
+  int K;                // CAS gradient k-chunks (trstmi_kchunks)
+};
+
+// CAS gradient chunk count K for a CTA of S threads: one
+// thread per (chunk, column), K = clamp(S / N, 1, 8).
+__host__ __device__ inline int kchunks_for(int d, int N, int S) {
+  (void)d;
+  const int K = S / N;
+  return K < 1 ? 1 : (K > 8 ? 8 : K);
+}
+
 // ------------------------------------------------------------------ CTA reductions
-// CAS sum: lanes already hold their strided partials; xor butterfly inside
-// each warp, then the S/32 warp totals left to right.  Result is identical in
-// every thread.  Two alternating scratch buffers make one __syncthreads per
-// reduction sufficient.
+// CAS sum: lanes hold their strided partials; xor butterfly inside each warp
+// (16,8,4,2,1), then the same butterfly across the S/32 warp totals (1,2,4,..)
+// — a pairwise tree in warp order.  Every thread ends with the identical sum.
+// Two alternating scratch buffers make one __syncthreads per reduction enough.
+template <int S>
+__device__ __forceinline__ double warp_tree_sum(const double* buf) {
+  constexpr int W = S / 32;
+  const int lane = threadIdx.x & 31;
+  double t = lane < W ? buf[lane] : 0.0;
+#pragma unroll
+  for (int off = 1; off < W; off <<= 1) t = __dadd_rn(t, __shfl_xor_sync(FULL, t, off));
+  return __shfl_sync(FULL, t, 0);
+}
+
 template <int S, int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& rbuf) {
   constexpr int W = S / 32;
@@ -55,12 +92,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& rbuf
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double t = buf[k * W];
-#pragma unroll
-      for (int w = 1; w < W; ++w) t = __dadd_rn(t, buf[k * W + w]);
-      v[k] = t;
-    }
+    for (int k = 0; k < K; ++k) v[k] = warp_tree_sum<S>(buf + k * W);
     rbuf ^= 1;
   } else {
     __syncwarp();
@@ -83,9 +115,11 @@ __device__ __forceinline__ double block_max(double v, double* red, int& rbuf) {
     double* buf = red + rbuf * (4 * W);
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
     __syncthreads();
-    v = buf[0];
+    const int lane = threadIdx.x & 31;
+    v = lane < W ? buf[lane] : buf[0];
 #pragma unroll
-    for (int w = 1; w < W; ++w) v = fmax(v, buf[w]);
+    for (int off = 1; off < W; off <<= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+    v = __shfl_sync(FULL, v, 0);
     rbuf ^= 1;
   } else {
     __syncwarp();
@@ -102,9 +136,8 @@ __device__ __forceinline__ int block_min_int(int v, int* ired, int& ibuf) {
     int* buf = ired + ibuf * W;
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
     __syncthreads();
-    v = buf[0];
-#pragma unroll
-    for (int w = 1; w < W; ++w) v = min(v, buf[w]);
+    const int lane = threadIdx.x & 31;
+    v = static_cast<int>(__reduce_min_sync(FULL, static_cast<unsigned>(lane < W ? buf[lane] : buf[0])));
     ibuf ^= 1;
   } else {
     __syncwarp();
@@ -159,22 +192,140 @@ __device__ __forceinline__ double dot_partial(const double* a, const double* b, 
 }
 
 // ------------------------------------------------------------------ pair walk
-// Row-major upper-triangular pair p -> (j, k); advancing by S stays O(1).
-__device__ __forceinline__ void pair_first(int N, int p, int& j, int& k) {
-  j = 0;
-  int row = N - 1;
-  while (p >= row) {
-    p -= row;
-    ++j;
-    --row;
-  }
-  k = j + 1 + p;
+// Row-major upper-triangular pair p = rowstart(j) + (k - j - 1).
+__device__ __forceinline__ int rowstart(int N, int j) { return j * N - j * (j + 1) / 2; }
+
+__device__ __forceinline__ void pair_of(int N, int p, int& j, int& k) {
+  const double b = 2.0 * N - 1.0;
+  int jj = (int)floor(0.5 * (b - sqrt(fmax(b * b - 8.0 * p, 0.0))));
+  jj = max(0, min(jj, N - 2));
+  while (jj < N - 2 && rowstart(N, jj + 1) <= p) ++jj;
+  while (jj > 0 && rowstart(N, jj) > p) --jj;
+  j = jj;
+  k = p - rowstart(N, jj) + jj + 1;
 }
-__device__ __forceinline__ void pair_advance(int N, int step, int& j, int& k) {
-  k += step;
-  while (k >= N && j < N - 1) {
-    k = k - N + (j + 2);
+
+// Warp-contiguous walk over all pairs: warp w owns the contiguous range
+// [w*chunk, (w+1)*chunk), lanes step by 32 (consecutive k within a row, so
+// the k-column reads are bank-conflict free).  f(p, j, k).
+template <int S, class F>
+__device__ __forceinline__ void for_pairs(int N, int n, F&& f) {
+  constexpr int W = S / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int chunk = (n + W - 1) / W;
+  const int pend = min(n, (warp + 1) * chunk);
+  int p = warp * chunk + lane;
+  if (p >= pend) return;
+  int j, k;
+  pair_of(N, p, j, k);
+  for (; p < pend; p += 32) {
+    f(p, j, k);
+    k += 32;
+    while (k >= N && j < N - 2) {
+      k = k - N + j + 2;
+      ++j;
+    }
+  }
+}
+
+// Same walk, four pairs per step (p, p+32, p+64, p+96) so the four
+// independent dependency chains interleave.  f(p[4], j[4], k[4], valid[4]).
+__device__ __forceinline__ void adv32(int N, int& j, int& k) {
+  k += 32;
+  while (k >= N && j < N - 2) {
+    k = k - N + j + 2;
     ++j;
+  }
+}
+template <int S, class F>
+__device__ __forceinline__ void for_pairs4(int N, int n, F&& f) {
+  constexpr int W = S / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int chunk = (n + W - 1) / W;
+  const int pend = min(n, (warp + 1) * chunk);
+  int p0 = warp * chunk + lane;
+  if (p0 >= pend) return;
+  int j0, k0;
+  pair_of(N, p0, j0, k0);
+  for (; p0 < pend; p0 += 128) {
+    int p[4], j[4], k[4];
+    bool v[4];
+    p[0] = p0;
+    j[0] = j0;
+    k[0] = k0;
+#pragma unroll
+    for (int u = 1; u < 4; ++u) {
+      j[u] = j[u - 1];
+      k[u] = k[u - 1];
+      adv32(N, j[u], k[u]);
+      p[u] = p[u - 1] + 32;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = p[u] < pend;
+      if (!v[u]) {  // keep indices in range; results are discarded
+        p[u] = p[0];
+        j[u] = j[0];
+        k[u] = k[0];
+      }
+    }
+    f(p, j, k, v);
+    j0 = j[3];
+    k0 = k[3];
+    adv32(N, j0, k0);
+  }
+}
+
+// Table-driven walk (the (j,k) of every pair is precomputed once per kernel
+// in Smem::jk as j | k << 16): warp-contiguous ranges, lanes step by 32,
+// four pairs per step.  f(p[4], j[4], k[4], valid[4]).
+template <int S, bool NEED_JK, class F>
+__device__ __forceinline__ void pairs4(int n, const unsigned* __restrict__ jk, F&& f) {
+  constexpr int W = S / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int chunk = (n + W - 1) / W;
+  const int pbeg = warp * chunk;
+  const int pend = min(n, pbeg + chunk);
+  for (int p0 = pbeg + lane; p0 < pend; p0 += 128) {
+    int p[4], j[4], k[4];
+    bool v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[u] = p0 + 32 * u < pend;
+      p[u] = v[u] ? p0 + 32 * u : p0;
+      if constexpr (NEED_JK) {
+        const unsigned t = jk[p[u]];
+        j[u] = (int)(t & 0xffffu);
+        k[u] = (int)(t >> 16);
+      } else {
+        j[u] = k[u] = 0;
+      }
+    }
+    f(p, j, k, v);
+  }
+}
+
+// CAS Gram entry G(j,k), j<k, from component-major phiS.
+template <bool CPLX, int DMAX, bool EXACT>
+__device__ __forceinline__ void gram_jk(const double* __restrict__ phiS, int N, int d_rt, int j, int k, double& re,
+                                        double& im) {
+  const int d = EXACT ? DMAX : d_rt;
+  re = 0.0;
+  im = 0.0;
+#pragma unroll
+  for (int i = 0; i < DMAX; ++i) {
+    if (i < d) {
+      if constexpr (CPLX) {
+        const double ar = phiS[(2 * i) * N + j], ai = phiS[(2 * i + 1) * N + j];
+        const double br = phiS[(2 * i) * N + k], bi = phiS[(2 * i + 1) * N + k];
+        re = fma(ar, br, re);
+        re = fma(ai, bi, re);
+        im = fma(ar, bi, im);
+        im = fma(-ai, br, im);
+      } else {
+        re = fma(phiS[i * N + j], phiS[i * N + k], re);
+      }
+    }
   }
 }
 
@@ -193,64 +344,35 @@ __device__ __forceinline__ double div_rn(double a, double b, double yb) {
 
 // ------------------------------------------------------------------ workspace
 // Shared-memory carve for one CTA.  phiS is component-major (phiS[q*N + j])
-// so a warp reading consecutive columns is bank-conflict free.  Per pair p:
-//   X[p]  : x_p (phase 2) -> w_p (phase 3) -> c_p*u_p, or -1 when c_p == 0
-//   GR[p] : Re G(j,k)     -> c_p * Re G(j,k)
-//   GI[p] : Im G(j,k)     -> c_p * Im G(j,k)      (complex frames only)
+// so a warp reading consecutive columns is bank-conflict free; a warp whose
+// lanes all read the same column gets a broadcast.
+//   U[p]  : x_p (phase 2) -> w_p (phase 3a) -> c_p = w_p / z (phase 3b)
+//   part  : K x N x (L+1) chunk partials of the gradient GEMM and of t
+//   mask  : N x NW words, bit k of column m set iff c(m,k) != 0 (sparse only)
 struct Smem {
-  double* phiS;   // L*N
-  double* alpha;  // N
-  double* X;      // n
-  double* GR;     // n
-  double* GI;     // n (complex) / 0 (real)
-  double* red;    // 2 * 4 * W
-  double* scal;   // 4 scalars (F of the last evaluation, ...)
-  int* ired;      // 2 * W
+  double* phiS;      // L*N
+  double* alpha;     // N
+  double* U;         // n
+  double* part;      // K*N*(L+1)
+  unsigned* mask;    // N*NW
+  unsigned* jk;      // n: pair p -> j | k << 16
+  double* red;       // 2 * 4 * W
+  double* scal;      // 4 scalars (F of the last evaluation, ...)
+  int* ired;         // 2 * W
 };
 
+__host__ __device__ inline int mask_words(int N) { return (N + 31) / 32; }
 __host__ __device__ inline long long pair_smem_doubles(const Prob& P, bool cplx) {
-  return (long long)P.n * (cplx ? 3 : 2);
+  (void)cplx;
+  return (long long)P.n + (long long)P.K * P.N * (P.L + 1) + ((long long)P.N * mask_words(P.N) + 1) / 2 +
+         ((long long)P.n + 1) / 2;
 }
 
-// Gram of the upper triangle, row by row: warp w takes row pairs (a, N-2-a)
-// (N pairs per row pair), lanes walk k.  Calls f(p, re, im) per pair.
-template <bool CPLX, int DMAX, bool EXACT, int S, class F>
-__device__ __forceinline__ void gram_rows(const Prob& P, const double* __restrict__ phiS, F&& f) {
-  constexpr int W = S / 32;
-  const int d = EXACT ? DMAX : P.d;
-  const int N = P.N;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nrp = N / 2;
-  for (int rp = warp; rp < nrp; rp += W) {
-#pragma unroll 1
-    for (int side = 0; side < 2; ++side) {
-      const int j = side == 0 ? rp : N - 2 - rp;
-      if (side == 1 && j <= rp) break;
-      double a[(CPLX ? 2 : 1) * DMAX];
-#pragma unroll
-      for (int q = 0; q < (CPLX ? 2 : 1) * DMAX; ++q)
-        a[q] = (q < (CPLX ? 2 : 1) * d) ? phiS[q * N + j] : 0.0;
-      const int base = j * N - j * (j + 1) / 2 - j - 1;
-      for (int k = j + 1 + lane; k < N; k += 32) {
-        double re = 0.0, im = 0.0;
-#pragma unroll
-        for (int i = 0; i < DMAX; ++i) {
-          if (i < d) {
-            if constexpr (CPLX) {
-              const double br = phiS[(2 * i) * N + k], bi = phiS[(2 * i + 1) * N + k];
-              re = fma(a[2 * i], br, re);
-              re = fma(a[2 * i + 1], bi, re);
-              im = fma(a[2 * i], bi, im);
-              im = fma(-a[2 * i + 1], br, im);
-            } else {
-              re = fma(a[i], phiS[i * N + k], re);
-            }
-          }
-        }
-        f(base + k, re, im);
-      }
-    }
-  }
+// Fills Smem::jk (once per kernel; ends with a barrier).
+template <int S>
+__device__ __forceinline__ void build_pair_table(const Prob& P, unsigned* jk) {
+  for_pairs<S>(P.N, P.n, [&](int p, int j, int k) { jk[p] = (unsigned)j | ((unsigned)k << 16); });
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ evaluation
@@ -258,22 +380,32 @@ __device__ __forceinline__ void gram_rows(const Prob& P, const double* __restric
 // CTA-wide.  Returns -1 or the first zero column (then *F = +inf and gout = 0,
 // the make_objective convention, solver.hpp:108-112).  gout may alias nothing
 // that is read here.  Ends with a __syncthreads().
-template <bool CPLX, int DMAX, bool EXACT, int S>
+//
+// Data movement: the only per-pair value kept in shared memory is one double
+// (x -> w -> c); the gradient recomputes G(k,m) in registers from phi_m
+// (registers) and phi_k (a shared-memory broadcast: every lane of a warp is at
+// the same k), so the FP64 pipe, not shared-memory bandwidth, sets the pace.
+// Pairs with c == 0 contribute exactly nothing (accumulators start at +0 and
+// never become -0), so skipping them is bit-identical to including them.
+template <bool CPLX, int DMAX, bool EXACT, int S, bool SQ = true>
 __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const double* __restrict__ dir, double sc,
-                        double delta, bool squared, const Smem& sm, int& rbuf, double* __restrict__ gout,
-                        double* F_out, double* s_out, double* __restrict__ wout) {
+                        double delta, const Smem& sm, int& rbuf, double* __restrict__ gout, double* F_out,
+                        double* s_out, double* __restrict__ wout) {
   constexpr int C = CPLX ? 2 : 1;
+  constexpr int LM = C * DMAX;
   const int d = EXACT ? DMAX : P.d;
   const int N = P.N, L = P.L, n = P.n;
   const int tid = threadIdx.x;
+  const int NW = mask_words(N);
+  PHASE_START;
 
   // ---- phase 1: column norms, normalisation (smoothing.hpp:95-102)
   int zc = INT_MAX;
   for (int j = tid; j < N; j += S) {
-    double col[C * DMAX];
+    double col[LM];
     double acc = 0.0;
 #pragma unroll
-    for (int q = 0; q < C * DMAX; ++q) {
+    for (int q = 0; q < LM; ++q) {
       if (q < C * d) {
         const double xv = x[j * L + q];
         const double pv = (sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(sc, dir[j * L + q]));
@@ -288,11 +420,12 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
     } else {
       const double ya = __drcp_rn(a);
 #pragma unroll
-      for (int q = 0; q < C * DMAX; ++q)
+      for (int q = 0; q < LM; ++q)
         if (q < C * d) sm.phiS[q * N + j] = div_rn(col[q], a, ya);
     }
   }
   zc = block_min_int<S>(zc, sm.ired, rbuf);  // also publishes phiS / alpha
+  PHASE_MARK(0);
   if (zc != INT_MAX) {
     for (int i = tid; i < P.dim; i += S) gout[i] = 0.0;
     if (F_out) *F_out = __longlong_as_double(0x7ff0000000000000LL);
@@ -303,95 +436,198 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
 
   // ---- phase 2: Gram upper triangle, x_p, s = max x_p (smoothing.hpp:104-118)
   double smax = -__longlong_as_double(0x7ff0000000000000LL);
-  gram_rows<CPLX, DMAX, EXACT, S>(P, sm.phiS, [&](int p, double re, double im) {
-    const double u = CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re);
-    const double xv = squared ? u : sqrt(u);
-    sm.X[p] = xv;
-    sm.GR[p] = re;
-    if constexpr (CPLX) sm.GI[p] = im;
-    smax = fmax(smax, xv);
+  pairs4<S, true>(n, sm.jk, [&](const int* p, const int* j, const int* k, const bool* v) {
+    double re[4], im[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) gram_jk<CPLX, DMAX, EXACT>(sm.phiS, N, d, j[u], k[u], re[u], im[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double uu = CPLX ? __dadd_rn(__dmul_rn(re[u], re[u]), __dmul_rn(im[u], im[u])) : __dmul_rn(re[u], re[u]);
+      double xv = uu;
+      if constexpr (!SQ) xv = sqrt(uu);
+      if (v[u]) {
+        sm.U[p[u]] = xv;
+        smax = xv > smax ? xv : smax;
+      }
+    }
   });
   const double s = block_max<S>(smax, sm.red, rbuf);
+  PHASE_MARK(1);
 
-  // ---- phase 3: w_p = exp((x_p - s)/delta), z = CAS sum (smoothing.hpp:119-126)
+  // ---- phase 3a: w_p = exp((x_p - s)/delta) (smoothing.hpp:119-124), any
+  // order; count the nonzero weights.  Clears the sparse-pattern mask.
+  for (int i = tid; i < N * NW; i += S) sm.mask[i] = 0u;
   const double cut = __dmul_rn(kUnderflowCut, delta);
   const double ydelta = __drcp_rn(delta);
-  double zp = 0.0;
-  for (int p = tid; p < n; p += S) {
-    const double diff = __dsub_rn(sm.X[p], s);
-    double w = 0.0;
-    if (diff >= cut) w = cas_exp(div_rn(diff, delta, ydelta));
-    sm.X[p] = w;
-    zp = __dadd_rn(zp, w);
-  }
-  const double z = block_sum1<S>(zp, sm.red, rbuf);
-  // ---- phase 3b: c_p = w_p / z and the pair coefficients of the gradient
-  // (smoothing.hpp:125, 136-142): c*u, c*Re G, c*Im G; c == 0 flagged -1.
-  const double yz = __drcp_rn(z);
-  for (int p = tid; p < n; p += S) {
-    const double w = sm.X[p];
-    const double c = (w == 0.0) ? 0.0 : div_rn(w, z, yz);
-    if (wout) wout[p] = c;
-    if (c == 0.0) {
-      sm.X[p] = -1.0;
+  double nnz = 0.0;
+  pairs4<S, false>(n, sm.jk, [&](const int* p, const int*, const int*, const bool* v) {
+    double diff[4], w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) diff[u] = __dsub_rn(sm.U[p[u]], s);
+    const bool any = (diff[0] >= cut) | (diff[1] >= cut) | (diff[2] >= cut) | (diff[3] >= cut);
+    if (any) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = (diff[u] >= cut) ? cas_exp(div_rn(diff[u], delta, ydelta)) : 0.0;
     } else {
-      const double gr = sm.GR[p];
-      const double gi = CPLX ? sm.GI[p] : 0.0;
-      const double u = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
-      double cc = c;
-      if (!squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(u), 1e-150)));
-      sm.X[p] = __dmul_rn(cc, u);
-      sm.GR[p] = __dmul_rn(cc, gr);
-      if constexpr (CPLX) sm.GI[p] = __dmul_rn(cc, gi);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = 0.0;
     }
-  }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (v[u]) {
+        sm.U[p[u]] = w[u];
+        if (w[u] != 0.0) nnz += 1.0;
+      }
+    }
+  });
+  __syncthreads();
+  PHASE_MARK(2);
+  // ---- phase 3z: z = CAS sum of w in lane-strided pair order (smoothing.hpp:121-124)
+  double zz[2] = {0.0, nnz};
+  for (int p = tid; p < n; p += S) zz[0] = __dadd_rn(zz[0], sm.U[p]);
+  block_sum<S, 2>(zz, sm.red, rbuf);
+  PHASE_MARK(3);
+  const double z = zz[0];
+  const bool sparse = zz[1] * 4.0 < (double)n;
+  // ---- phase 3b: c_p = w_p / z (smoothing.hpp:125); sparse pattern mask
+  const double yz = __drcp_rn(z);
+  auto coef = [&](const int* p, const int* j, const int* k, const bool* v) {
+    double w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = sm.U[p[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double c = (w[u] == 0.0) ? 0.0 : div_rn(w[u], z, yz);
+      if (v[u]) {
+        if (wout) wout[p[u]] = c;
+        if (w[u] != 0.0) sm.U[p[u]] = c;
+        if (sparse && c != 0.0) {
+          atomicOr(&sm.mask[j[u] * NW + (k[u] >> 5)], 1u << (k[u] & 31));
+          atomicOr(&sm.mask[k[u] * NW + (j[u] >> 5)], 1u << (j[u] & 31));
+        }
+      }
+    }
+  };
+  if (sparse) pairs4<S, true>(n, sm.jk, coef);
+  else pairs4<S, false>(n, sm.jk, coef);
   if (F_out && tid == 0) *F_out = __dadd_rn(s, __dmul_rn(delta, cas_log(z)));
   if (s_out && tid == 0) *s_out = s;
   __syncthreads();
+  PHASE_MARK(4);
 
-  // ---- phase 4: gradient (smoothing.hpp:147-160).  One thread per output
-  // component (m, i): k ascending, pairs with c == 0 skipped, G(k,m) =
-  // conj(G(m,k)) for k > m.  t_m is recomputed by each of column m's threads.
-  for (int unit = tid; unit < N * d; unit += S) {
-    const int m = unit / d;
-    const int i = unit - m * d;
-    double acc_re = 0.0, acc_im = 0.0, t = 0.0;
-    int plo = m - 1;                                   // p(k, m) for k = 0
-    const int prow = m * N - m * (m + 1) / 2 - m - 1;  // p(m, k) = prow + k
-    const double* pkr = sm.phiS + (C * i) * N;
-    const double* pki = sm.phiS + (C * i + 1) * N;
-    for (int k = 0; k < N; ++k) {
-      if (k == m) continue;
-      const bool lower = k < m;
-      const int p = lower ? plo : prow + k;
-      if (lower) plo += N - k - 2;
-      const double cu = sm.X[p];
-      if (cu < 0.0) continue;  // c == 0
-      t = __dadd_rn(t, cu);
-      const double cr = sm.GR[p];
-      const double pr = pkr[k];
-      if constexpr (CPLX) {
-        const double gi = sm.GI[p];
-        const double ci = lower ? gi : -gi;
-        const double pi = pki[k];
-        acc_re = fma(pr, cr, acc_re);
-        acc_re = fma(-pi, ci, acc_re);
-        acc_im = fma(pr, ci, acc_im);
-        acc_im = fma(pi, cr, acc_im);
-      } else {
-        acc_re = fma(pr, cr, acc_re);
+  // ---- phase 4: gradient (smoothing.hpp:130-160), CAS chunked order.
+  // Thread (chunk ch, column m): ascending k in [ch*N/K, (ch+1)*N/K):
+  // G(k,m) recomputed (CAS gram order on (min, max), conjugated for k > m),
+  // t += c*u, acc += phi_k * (c G).  Partials go to part[], then each output
+  // adds its K partials left to right.
+  const int K = P.K;
+  for (int unit = tid; unit < K * N; unit += S) {
+    const int ch = unit / N;
+    const int m = unit - ch * N;
+    const int k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
+    double pm[LM], acc[LM];
+#pragma unroll
+    for (int q = 0; q < LM; ++q) {
+      pm[q] = (q < C * d) ? sm.phiS[q * N + m] : 0.0;
+      acc[q] = 0.0;
+    }
+    double tp = 0.0;
+    auto term = [&](int k, double c, auto lower_tag) {
+      constexpr bool lower = decltype(lower_tag)::value;
+      double pk[LM];
+#pragma unroll
+      for (int q = 0; q < LM; ++q) pk[q] = (q < C * d) ? sm.phiS[q * N + k] : 0.0;
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int i = 0; i < DMAX; ++i) {
+        if (i < d) {
+          if constexpr (CPLX) {
+            const double ar = lower ? pk[2 * i] : pm[2 * i], ai = lower ? pk[2 * i + 1] : pm[2 * i + 1];
+            const double br = lower ? pm[2 * i] : pk[2 * i], bi = lower ? pm[2 * i + 1] : pk[2 * i + 1];
+            re = fma(ar, br, re);
+            re = fma(ai, bi, re);
+            im = fma(ar, bi, im);
+            im = fma(-ai, br, im);
+          } else {
+            re = fma(pk[i], pm[i], re);
+          }
+        }
+      }
+      const double gr = re;
+      const double gi = lower ? im : -im;  // G(k,m)
+      const double uu = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+      double cc = c;
+      if constexpr (!SQ) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(uu), 1e-150)));
+      tp = __dadd_rn(tp, __dmul_rn(cc, uu));
+      const double cr = __dmul_rn(cc, gr);
+      const double ci = __dmul_rn(cc, gi);
+#pragma unroll
+      for (int i = 0; i < DMAX; ++i) {
+        if (i < d) {
+          if constexpr (CPLX) {
+            acc[2 * i] = fma(pk[2 * i], cr, acc[2 * i]);
+            acc[2 * i] = fma(-pk[2 * i + 1], ci, acc[2 * i]);
+            acc[2 * i + 1] = fma(pk[2 * i], ci, acc[2 * i + 1]);
+            acc[2 * i + 1] = fma(pk[2 * i + 1], cr, acc[2 * i + 1]);
+          } else {
+            acc[i] = fma(pk[i], cr, acc[i]);
+          }
+        }
+      }
+    };
+    if (sparse) {
+      const unsigned* mrow = sm.mask + m * NW;
+      for (int wi = k_lo >> 5; wi <= ((k_hi - 1) >> 5); ++wi) {
+        unsigned wd = mrow[wi];
+        const int base = wi << 5;
+        if (base < k_lo) wd &= ~0u << (k_lo - base);
+        if (k_hi - base < 32) wd &= (1u << (k_hi - base)) - 1u;
+        while (wd) {
+          const int k = base + __ffs(wd) - 1;
+          wd &= wd - 1;
+          if (k < m) term(k, sm.U[rowstart(N, k) + (m - k - 1)], BoolTag<true>{});
+          else term(k, sm.U[rowstart(N, m) + (k - m - 1)], BoolTag<false>{});
+        }
+      }
+    } else {
+      const int kA = min(k_hi, m);
+      if (k_lo < kA) {
+        int plo = rowstart(N, k_lo) + (m - k_lo - 1);
+        for (int k = k_lo; k < kA; ++k) {
+          const double c = sm.U[plo];
+          plo += N - k - 2;
+          if (c != 0.0) term(k, c, BoolTag<true>{});
+        }
+      }
+      const int kB = max(k_lo, m + 1);
+      const int prow = rowstart(N, m) - m - 1;  // p(m, k) = prow + k
+      for (int k = kB; k < k_hi; ++k) {
+        const double c = sm.U[prow + k];
+        if (c != 0.0) term(k, c, BoolTag<false>{});
       }
     }
-    const double am = sm.alpha[m];
-    const double ya = __drcp_rn(am);
-    const double pmr = sm.phiS[(C * i) * N + m];
-    gout[m * L + C * i] = __dmul_rn(div_rn(__dsub_rn(acc_re, __dmul_rn(t, pmr)), am, ya), 2.0);
-    if constexpr (CPLX) {
-      const double pmi = sm.phiS[(C * i + 1) * N + m];
-      gout[m * L + C * i + 1] = __dmul_rn(div_rn(__dsub_rn(acc_im, __dmul_rn(t, pmi)), am, ya), 2.0);
-    }
+    double* pp = sm.part + (long long)unit * (L + 1);
+#pragma unroll
+    for (int q = 0; q < LM; ++q)
+      if (q < C * d) pp[q] = acc[q];
+    pp[L] = tp;
   }
   __syncthreads();
+  for (int mq = tid; mq < N * L; mq += S) {
+    const int m = mq / L;
+    const int q = mq - m * L;
+    double a = 0.0, t = 0.0;
+    for (int ch = 0; ch < K; ++ch) {
+      const double* pp = sm.part + (long long)(ch * N + m) * (L + 1);
+      a = ch == 0 ? pp[q] : __dadd_rn(a, pp[q]);
+      t = ch == 0 ? pp[L] : __dadd_rn(t, pp[L]);
+    }
+    const double am = sm.alpha[m];
+    gout[m * L + q] =
+        __dmul_rn(div_rn(__dsub_rn(a, __dmul_rn(t, sm.phiS[q * N + m])), am, __drcp_rn(am)), 2.0);
+  }
+  __syncthreads();
+  PHASE_MARK(5);
   return -1;
 }
 
@@ -428,11 +664,17 @@ __device__ int coherence_cta(const Prob& P, const double* __restrict__ f, bool n
   if (zc != INT_MAX) return zc;
   double best = 0.0;
   long long arg = LLONG_MAX;
-  gram_rows<CPLX, DMAX, EXACT, S>(P, sm.phiS, [&](int p, double re, double im) {
-    const double m = sqrt(CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re));
-    if (m > best || (m == best && m > 0.0 && p < arg)) {
-      best = m;
-      arg = p;
+  pairs4<S, true>(P.n, sm.jk, [&](const int* p, const int* j, const int* k, const bool* v) {
+    double re[4], im[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) gram_jk<CPLX, DMAX, EXACT>(sm.phiS, N, d, j[u], k[u], re[u], im[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double m = sqrt(CPLX ? __dadd_rn(__dmul_rn(re[u], re[u]), __dmul_rn(im[u], im[u])) : __dmul_rn(re[u], re[u]));
+      if (v[u] && m > best) {  // pairs ascend within a thread: first strict maximum
+        best = m;
+        arg = p[u];
+      }
     }
   });
   block_argmax<S>(best, arg, sm.red, rbuf);

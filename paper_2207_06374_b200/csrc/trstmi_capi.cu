@@ -95,6 +95,7 @@ Prob make_prob(int field, long long d, long long N) {
   P.L = (field == TRSTMI_COMPLEX ? 2 : 1) * (int)d;
   P.dim = P.L * P.N;
   P.n = (int)(N * (N - 1) / 2);
+  P.K = kchunks_for(P.d, P.N, trstmi_lanes(field, d, N));
   return P;
 }
 
@@ -176,11 +177,13 @@ int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t
   return TRSTMI_OK;
 }
 
+int trstmi_kchunks(int field, int64_t d, int64_t N) { return kchunks_for((int)d, (int)N, trstmi_lanes(field, d, N)); }
+
 int trstmi_lanes(int field, int64_t d, int64_t N) {
   const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
   const long long n = N * (N - 1) / 2;
+  (void)n;
   if (dim <= 64) return 32;
-  if (n >= 2048) return 512;
   if (dim <= 256) return 128;
   return 256;
 }
@@ -300,7 +303,7 @@ int trstmi_eval_batch_dev(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int6
   A.weights = weights;
   A.zero_col = reinterpret_cast<long long*>(zero_col);
   cudaSetDevice(ctx->device);
-  return batch_launch(ctx, 0, field, d, N, A, stream ? (cudaStream_t)stream : ctx->stream);
+  return batch_launch(ctx, 0, field, d, N, A, (cudaStream_t)stream);
 }
 
 int trstmi_eval_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B, const double* pts,
@@ -483,7 +486,7 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
   int rc = resolve_cfg(ctx, cfg, A, sched);
   if (rc) return rc;
   cudaSetDevice(ctx->device);
-  cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+  cudaStream_t st = (cudaStream_t)stream;
   A.n_list = (int)trials;
   A.params = params_dev;
   A.frames = frames_dev;

@@ -68,16 +68,20 @@ def _py_cas_sum(v, S, dot_with=None):
             lane[p % S] = lane[p % S] + x
         else:
             lane[p % S] = _fma(x, dot_with[p], lane[p % S])
-    total = None
+    tot = []
     for w in range(S // 32):
         a = lane[32 * w:32 * w + 32]
         for off in (16, 8, 4, 2, 1):
             a = [a[l] + a[l ^ off] for l in range(32)]
-        total = a[0] if total is None else total + a[0]
-    return total
+        tot.append(a[0])
+    off = 1
+    while off < len(tot):
+        tot = [tot[w] + tot[w ^ off] for w in range(len(tot))]
+        off *= 2
+    return tot[0]
 
 
-@pytest.mark.parametrize("S", [32, 128, 256])
+@pytest.mark.parametrize("S", [32, 128, 256, 512])
 def test_cas_reduction_shape(S):
     rng = np.random.default_rng(S)
     for n in (1, 31, 400, 4950):
