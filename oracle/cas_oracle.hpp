@@ -103,11 +103,9 @@ inline double pow2i(int k) {  // 2^k for -1022 <= k <= 1023, exact
 }
 
 inline double cas_exp(double x) {
-  if (!(x == x)) return x;
-  if (x > 709.782712893383973096) return std::numeric_limits<double>::infinity();
-  if (x < -745.2) return 0.0;
-  const double kd = std::nearbyint(x * 1.4426950408889634);
-  double r = std::fma(-kd, 6.93147180369123816490e-01, x);
+  const double xc = std::fmin(std::fmax(x, -745.25), 709.8);
+  const double kd = std::nearbyint(xc * 1.4426950408889634);
+  double r = std::fma(-kd, 6.93147180369123816490e-01, xc);
   r = std::fma(-kd, 1.90821492927058770002e-10, r);
   double p = 1.6059043836821613e-10;            // 1/13!
   p = std::fma(p, r, 2.08767569878680989792e-09);  // 1/12!
@@ -124,9 +122,11 @@ inline double cas_exp(double x) {
   p = std::fma(p, r, 1.0);
   p = std::fma(p, r, 1.0);
   const int k = static_cast<int>(kd);
-  if (k > 1000) return (p * pow2i(k - 64)) * 0x1.0p64;
-  if (k < -1000) return (p * pow2i(k + 600)) * 0x1.0p-600;
-  return p * pow2i(k);
+  const int k1 = k >> 1;  // arithmetic shift: floor(k / 2)
+  double res = (p * pow2i(k1)) * pow2i(k - k1);  // exact, then one rounding
+  if (x > 709.782712893383973096) res = std::numeric_limits<double>::infinity();
+  if (x < -745.2) res = 0.0;
+  return (x == x) ? res : x;
 }
 
 // CAS log (used once per evaluation, for F = s + delta*log z with z >= 1):

@@ -17,12 +17,14 @@ __device__ __forceinline__ double pow2i(int k) {  // 2^k, -1022 <= k <= 1023
   return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
 
+// Branch-free so that several independent exps interleave in one thread.
+// The final scaling p * 2^k is done as (p * 2^(k>>1)) * 2^(k - (k>>1)): the
+// first product is exact, the second rounds once, so every result (normal,
+// subnormal or overflowing) is RN(p * 2^k).
 __device__ __forceinline__ double cas_exp(double x) {
-  if (!(x == x)) return x;
-  if (x > 709.782712893383973096) return __longlong_as_double(0x7ff0000000000000LL);
-  if (x < -745.2) return 0.0;
-  const double kd = rint(__dmul_rn(x, 1.4426950408889634));
-  double r = fma(-kd, 6.93147180369123816490e-01, x);
+  const double xc = fmin(fmax(x, -745.25), 709.8);
+  const double kd = rint(__dmul_rn(xc, 1.4426950408889634));
+  double r = fma(-kd, 6.93147180369123816490e-01, xc);
   r = fma(-kd, 1.90821492927058770002e-10, r);
   double p = 1.6059043836821613e-10;
   p = fma(p, r, 2.08767569878680989792e-09);
@@ -39,9 +41,11 @@ __device__ __forceinline__ double cas_exp(double x) {
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const int k = static_cast<int>(kd);
-  if (k > 1000) return __dmul_rn(__dmul_rn(p, pow2i(k - 64)), 0x1.0p64);
-  if (k < -1000) return __dmul_rn(__dmul_rn(p, pow2i(k + 600)), 0x1.0p-600);
-  return __dmul_rn(p, pow2i(k));
+  const int k1 = k >> 1;
+  double res = __dmul_rn(__dmul_rn(p, pow2i(k1)), pow2i(k - k1));
+  res = (x > 709.782712893383973096) ? __longlong_as_double(0x7ff0000000000000LL) : res;
+  res = (x < -745.2) ? 0.0 : res;
+  return (x == x) ? res : x;
 }
 
 __device__ __forceinline__ double cas_log(double x) {

@@ -341,6 +341,14 @@ __device__ __forceinline__ double div_rn(double a, double b, double yb) {
   const double r = fma(-q0, b, a);
   return fma(r, yb, q0);
 }
+// Branch-free Markstein quotient, valid when |a| >= 2^-900 or a == 0; the
+// caller fixes up the (rare) tiny numerators with div_needs_ieee().
+__device__ __forceinline__ double div_fast(double a, double b, double yb) {
+  const double q0 = __dmul_rn(a, yb);
+  const double r = fma(-q0, b, a);
+  return fma(r, yb, q0);
+}
+__device__ __forceinline__ bool div_needs_ieee(double a) { return a != 0.0 && fabs(a) < 0x1.0p-900; }
 
 // ------------------------------------------------------------------ workspace
 // Shared-memory carve for one CTA.  phiS is component-major (phiS[q*N + j])
@@ -466,8 +474,20 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
     for (int u = 0; u < 4; ++u) diff[u] = __dsub_rn(sm.U[p[u]], s);
     const bool any = (diff[0] >= cut) | (diff[1] >= cut) | (diff[2] >= cut) | (diff[3] >= cut);
     if (any) {
+      double y[4];
+      bool fix = false;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) w[u] = (diff[u] >= cut) ? cas_exp(div_rn(diff[u], delta, ydelta)) : 0.0;
+      for (int u = 0; u < 4; ++u) {
+        y[u] = div_fast(diff[u], delta, ydelta);
+        fix |= div_needs_ieee(diff[u]);
+      }
+      if (fix) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (div_needs_ieee(diff[u])) y[u] = __ddiv_rn(diff[u], delta);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = (diff[u] >= cut) ? cas_exp(y[u]) : 0.0;
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u) w[u] = 0.0;
@@ -492,12 +512,22 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
   // ---- phase 3b: c_p = w_p / z (smoothing.hpp:125); sparse pattern mask
   const double yz = __drcp_rn(z);
   auto coef = [&](const int* p, const int* j, const int* k, const bool* v) {
-    double w[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) w[u] = sm.U[p[u]];
+    double w[4], cq[4];
+    bool fix = false;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double c = (w[u] == 0.0) ? 0.0 : div_rn(w[u], z, yz);
+      w[u] = sm.U[p[u]];
+      cq[u] = div_fast(w[u], z, yz);
+      fix |= div_needs_ieee(w[u]);
+    }
+    if (fix) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (div_needs_ieee(w[u])) cq[u] = __ddiv_rn(w[u], z);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double c = cq[u];
       if (v[u]) {
         if (wout) wout[p[u]] = c;
         if (w[u] != 0.0) sm.U[p[u]] = c;
@@ -592,19 +622,19 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
     } else {
       const int kA = min(k_hi, m);
       if (k_lo < kA) {
+        // dense: branch-free (a c == 0 term adds exactly nothing)
         int plo = rowstart(N, k_lo) + (m - k_lo - 1);
+#pragma unroll 2
         for (int k = k_lo; k < kA; ++k) {
           const double c = sm.U[plo];
           plo += N - k - 2;
-          if (c != 0.0) term(k, c, BoolTag<true>{});
+          term(k, c, BoolTag<true>{});
         }
       }
       const int kB = max(k_lo, m + 1);
       const int prow = rowstart(N, m) - m - 1;  // p(m, k) = prow + k
-      for (int k = kB; k < k_hi; ++k) {
-        const double c = sm.U[prow + k];
-        if (c != 0.0) term(k, c, BoolTag<false>{});
-      }
+#pragma unroll 2
+      for (int k = kB; k < k_hi; ++k) term(k, sm.U[prow + k], BoolTag<false>{});
     }
     double* pp = sm.part + (long long)unit * (L + 1);
 #pragma unroll
