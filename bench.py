@@ -312,7 +312,9 @@ def main():
     prof = os.path.join(ROOT, "profiles", "anneal_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(args.config)
+            rec = json.load(open(prof)).get(args.config)
+            if rec:  # ncu dram read+write bytes per trial, scaled to this launch's trials
+                traffic = rec["bytes_per_trial"] * trials
         except Exception:
             traffic = None
 
@@ -341,7 +343,7 @@ def main():
         "best_mu": best_mu, "best_trial": gbest,
         "welch_bound": api.welch_bound(d, N),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": achieved / peak.value, "traffic": traffic,
+                     "frac": achieved / peak.value, "traffic": traffic, "traffic_unit": "bytes/launch",
                      "note": "achieved = evals x 16dN^2 (dense contraction count, SURVEY 8d) / anneal-kernel time; "
                              "peak = DFMA-loop throughput measured live on this GPU (MEASURED_PEAKS.json has no FP64)"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "cpu_baseline": cpu,

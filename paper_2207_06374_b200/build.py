@@ -73,7 +73,22 @@ def build(verbose=False, force=False, jobs=None):
     tmp = LIB + ".tmp"
     _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"])
     os.replace(tmp, LIB)
+    build_host_tests()
     return LIB
+
+
+HOST_TEST_SRC = os.path.join(HERE, "..", "tests", "cpp", "test_host_api.cpp")
+HOST_TEST_BIN = os.path.join(LIBDIR, "test_host_api")
+
+
+def build_host_tests():
+    """C++ host-mirror tests (tests/cpp), linked against the in-tree library."""
+    if not os.path.exists(HOST_TEST_SRC):
+        return None
+    gxx = shutil.which("g++") or "g++"
+    _run([gxx, "-std=c++17", "-O2", "-ffp-contract=off", "-o", HOST_TEST_BIN, HOST_TEST_SRC, "-L" + LIBDIR,
+          "-ltrstmi_b200", "-Wl,-rpath,$ORIGIN"])
+    return HOST_TEST_BIN
 
 
 if __name__ == "__main__":
