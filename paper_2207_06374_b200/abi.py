@@ -80,10 +80,7 @@ def dim_of(field, d, N):
 
 
 def lanes_for(field, d, N):
-    """CAS reduction width S; must equal trstmi_lanes() in csrc."""
-    dim = dim_of(field, d, N)
-    if dim <= 64:
-        return 32
-    if dim <= 256:
-        return 128
-    return 256
+    """CAS reduction width S — trstmi_lanes() of the built library
+    (a pure function; loading the library needs no GPU)."""
+    from . import api
+    return api.load_library().trstmi_lanes(field, d, N)

@@ -63,9 +63,10 @@ def build(verbose=False, force=False, jobs=None):
         objs.append(o)
         tasks.append(COMMON + ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-c",
                                os.path.join(CSRC, "instantiate.cu"), "-o", o])
-    o = os.path.join(BUILD, "trstmi_capi.o")
-    objs.append(o)
-    tasks.append(COMMON + ["-c", os.path.join(CSRC, "trstmi_capi.cu"), "-o", o])
+    for src in ("trstmi_capi.cu", "large_engine.cu"):
+        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        objs.append(o)
+        tasks.append(COMMON + ["-c", os.path.join(CSRC, src), "-o", o])
     with cf.ThreadPoolExecutor(jobs) as ex:
         for log in ex.map(lambda c: _run([NVCC] + c), tasks):
             if verbose and log.strip():

@@ -1,0 +1,477 @@
+// Large-frame path (BASELINE configs 4-5: real d=64 N=1024, complex d=128
+// N=4096, and any shape whose trial state does not fit one SM): one
+// evaluation is a short pipeline of grid-wide kernels over state in HBM/L2.
+//
+//   K1 large_normalize   alpha_j, phi = p/alpha (component-major), first zero column
+//   K2 large_gram        upper-triangular 64x64 register-tiled Gram (SYRK) ->
+//                        x_p, G(j,k) packed; s = max x_p (atomicMax on the bits)
+//   K3 large_weights     w_p = exp((x_p - s)/delta); lane partials of z
+//   K4 large_zreduce     z (CAS tree over the 128 CTA totals); F = s + delta log z
+//   K5 large_coef        c = w/z; dense coefficient matrices P = c G (k,m) and c u
+//   K6 large_grad_gemm   chunked D = Phi P (register-tiled DGEMM, CAS k-chunks)
+//   K6b large_tsum       t chunk partials
+//   K7 large_finalize    chunk combine, grad = ((acc - t phi)/alpha) * 2
+//
+// Arithmetic is the Canonical Arithmetic Spec with S = 32768
+// reduction lanes (128 CTAs x 256 threads) and K = clamp(S/N, 1, 8) gradient
+// chunks, so every value is bit-identical to the oracle run with the same S.
+// FP64 tensor cores are not used: sm_100a has no FP64 tcgen05 kind, and the
+// legacy DMMA peak equals the DFMA peak on B200 while its internal summation
+// order is unspecified — SIMT DFMA tiles keep the CAS order exact.
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "small_path.cuh"
+
+namespace trstmi_dev {
+
+constexpr int LS_CTAS = 128;
+constexpr int LS_THREADS = 256;
+constexpr int LS_LANES = LS_CTAS * LS_THREADS;  // 32768 CAS lanes
+constexpr int GT = 64;                           // Gram tile (pairs per side)
+constexpr int GIC = 8;                           // Gram i-rows staged per step
+
+struct LargeEval {
+  int cplx, d, N, L, dim, K, squared;
+  long long n;
+  const double* x;
+  const double* dir;
+  double sc, delta;
+  double* phiT;                    // L x N component-major
+  double* alpha;                   // N
+  int* zero_col;                   // 1
+  double* X;                       // n: x -> w
+  double* GR;                      // n
+  double* GI;                      // n
+  unsigned long long* smax_bits;   // 1
+  double* zpart;                   // LS_CTAS
+  double* scal;                    // [0] s, [1] z, [2] F
+  double* PR;                      // N x N
+  double* PI;                      // N x N
+  double* CU;                      // N x N
+  double* part;                    // K x dim
+  double* tpart;                   // K x N
+  double* gout;                    // dim
+  double* wout;                    // n or null
+};
+
+// ---- K1
+__global__ void large_normalize(LargeEval E) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *E.smax_bits = 0ull;
+  if (j >= E.N) return;
+  const int L = E.L;
+  double acc = 0.0;
+  for (int q = 0; q < L; ++q) {
+    const double xv = E.x[(long long)j * L + q];
+    const double pv = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[(long long)j * L + q]));
+    acc = fma(pv, pv, acc);
+  }
+  const double a = sqrt(acc);
+  E.alpha[j] = a;
+  if (a < kZeroColumnTol) {
+    atomicMin(E.zero_col, j);
+    return;
+  }
+  for (int q = 0; q < L; ++q) {
+    const double xv = E.x[(long long)j * L + q];
+    const double pv = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[(long long)j * L + q]));
+    E.phiT[(long long)q * E.N + j] = __ddiv_rn(pv, a);
+  }
+}
+
+__device__ __forceinline__ void tile_of(int t, int nt, int& jb, int& kb) {  // upper-triangular tile index
+  int row = 0, rem = t;
+  while (rem >= nt - row) {
+    rem -= nt - row;
+    ++row;
+  }
+  jb = row;
+  kb = row + rem;
+}
+
+// ---- K2: tile (jb <= kb) of GT x GT pairs, 256 threads x (4 j x 4 k).
+// mode 0: objective (store x, G, max); mode 1: coherence (per-tile max |G| and first argmax).
+template <bool CPLX, int MODE>
+__global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, long long* tile_arg) {
+  __shared__ double sa[2][GIC][GT];
+  __shared__ double sb[2][GIC][GT];
+  __shared__ double red_v[8];
+  __shared__ long long red_i[8];
+  const int N = E.N, d = E.d;
+  const int nt = (N + GT - 1) / GT;
+  int jb, kb;
+  tile_of(blockIdx.x, nt, jb, kb);
+  const int tid = threadIdx.x;
+  const int tj = tid >> 4, tk = tid & 15;  // 16 x 16 threads, each 4 j x 4 k (strided by 16)
+  double re[4][4], im[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) re[a][b] = im[a][b] = 0.0;
+  for (int i0 = 0; i0 < d; i0 += GIC) {
+    __syncthreads();
+    for (int e = tid; e < GIC * GT; e += 256) {
+      const int ii = e / GT, c = e - ii * GT;
+      const int i = i0 + ii;
+      const int j = jb * GT + c, k = kb * GT + c;
+      const bool iv = i < d;
+      sa[0][ii][c] = (iv && j < N) ? E.phiT[(long long)(CPLX ? 2 * i : i) * N + j] : 0.0;
+      sb[0][ii][c] = (iv && k < N) ? E.phiT[(long long)(CPLX ? 2 * i : i) * N + k] : 0.0;
+      if (CPLX) {
+        sa[1][ii][c] = (iv && j < N) ? E.phiT[(long long)(2 * i + 1) * N + j] : 0.0;
+        sb[1][ii][c] = (iv && k < N) ? E.phiT[(long long)(2 * i + 1) * N + k] : 0.0;
+      }
+    }
+    __syncthreads();
+    const int imax = min(GIC, d - i0);
+    for (int ii = 0; ii < imax; ++ii) {
+      double ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ar[a] = sa[0][ii][tj + 16 * a];
+        br[a] = sb[0][ii][tk + 16 * a];
+        if (CPLX) {
+          ai[a] = sa[1][ii][tj + 16 * a];
+          bi[a] = sb[1][ii][tk + 16 * a];
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (CPLX) {
+            re[a][b] = fma(ar[a], br[b], re[a][b]);
+            re[a][b] = fma(ai[a], bi[b], re[a][b]);
+            im[a][b] = fma(ar[a], bi[b], im[a][b]);
+            im[a][b] = fma(-ai[a], br[b], im[a][b]);
+          } else {
+            re[a][b] = fma(ar[a], br[b], re[a][b]);
+          }
+        }
+    }
+  }
+  double best = MODE == 0 ? 0.0 : 0.0;
+  long long barg = LLONG_MAX;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = jb * GT + tj + 16 * a, k = kb * GT + tk + 16 * b;
+      if (j < k && k < N) {
+        const long long p = (long long)j * N - (long long)j * (j + 1) / 2 + (k - j - 1);
+        const double u = CPLX ? __dadd_rn(__dmul_rn(re[a][b], re[a][b]), __dmul_rn(im[a][b], im[a][b]))
+                              : __dmul_rn(re[a][b], re[a][b]);
+        if (MODE == 0) {
+          const double xv = E.squared ? u : sqrt(u);
+          E.X[p] = xv;
+          E.GR[p] = re[a][b];
+          if (CPLX) E.GI[p] = im[a][b];
+          best = fmax(best, xv);
+        } else {
+          const double m = sqrt(u);
+          if (m > best || (m == best && m > 0.0 && p < barg)) {
+            best = m;
+            barg = p;
+          }
+        }
+      }
+    }
+  // CTA reduction
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const double ov = __shfl_xor_sync(FULL, best, off);
+    const long long oi = __shfl_xor_sync(FULL, barg, off);
+    if (ov > best || (ov == best && oi < barg)) {
+      best = ov;
+      barg = oi;
+    }
+  }
+  if ((tid & 31) == 0) {
+    red_v[tid >> 5] = best;
+    red_i[tid >> 5] = barg;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v = red_v[0];
+    long long ix = red_i[0];
+    for (int w = 1; w < 8; ++w)
+      if (red_v[w] > v || (red_v[w] == v && red_i[w] < ix)) {
+        v = red_v[w];
+        ix = red_i[w];
+      }
+    if (MODE == 0) {
+      atomicMax(E.smax_bits, (unsigned long long)__double_as_longlong(v));  // x >= 0: bit order == value order
+    } else {
+      tile_mu[blockIdx.x] = v;
+      tile_arg[blockIdx.x] = ix;
+    }
+  }
+}
+
+// ---- K3: weights and CAS lane partials of z (lane t = global thread id)
+__global__ void __launch_bounds__(LS_THREADS) large_weights(LargeEval E) {
+  __shared__ double wt[LS_THREADS / 32];
+  const double s = __longlong_as_double((long long)*E.smax_bits);
+  const double cut = __dmul_rn(kUnderflowCut, E.delta);
+  const long long t = (long long)blockIdx.x * LS_THREADS + threadIdx.x;
+  double zp = 0.0;
+  for (long long p = t; p < E.n; p += LS_LANES) {
+    const double diff = __dsub_rn(E.X[p], s);
+    const double w = (diff < cut) ? 0.0 : cas_exp(__ddiv_rn(diff, E.delta));
+    E.X[p] = w;
+    zp = __dadd_rn(zp, w);
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) zp = __dadd_rn(zp, __shfl_xor_sync(FULL, zp, off));
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = zp;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < LS_THREADS / 32 ? wt[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 1; off < LS_THREADS / 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+    if (threadIdx.x == 0) E.zpart[blockIdx.x] = v;
+    if (blockIdx.x == 0 && threadIdx.x == 0) E.scal[0] = s;
+  }
+}
+
+// ---- K4: z = pairwise tree over the CTA totals (continuing the warp tree)
+__global__ void large_zreduce(LargeEval E) {
+  __shared__ double wt[LS_CTAS / 32];
+  double v = E.zpart[threadIdx.x];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double u = threadIdx.x < LS_CTAS / 32 ? wt[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 1; off < LS_CTAS / 32; off <<= 1) u = __dadd_rn(u, __shfl_xor_sync(FULL, u, off));
+    if (threadIdx.x == 0) {
+      E.scal[1] = u;
+      E.scal[2] = __dadd_rn(E.scal[0], __dmul_rn(E.delta, cas_log(u)));
+    }
+  }
+}
+
+// ---- K5: coefficients into dense P (row k, column m): P(k,m) = c G(k,m)
+template <bool CPLX>
+__global__ void large_coef(LargeEval E) {
+  const double z = E.scal[1];
+  const int N = E.N;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < E.n; p += (long long)gridDim.x * blockDim.x) {
+    // pair -> (j, k)
+    const double b = 2.0 * N - 1.0;
+    long long j = (long long)floor(0.5 * (b - sqrt(fmax(b * b - 8.0 * (double)p, 0.0))));
+    j = max(0LL, min(j, (long long)N - 2));
+    while (j < N - 2 && (j + 1) * N - (j + 1) * (j + 2) / 2 <= p) ++j;
+    while (j > 0 && j * N - j * (j + 1) / 2 > p) --j;
+    const long long k = p - (j * N - j * (j + 1) / 2) + j + 1;
+    const double w = E.X[p];
+    const double c = (w == 0.0) ? 0.0 : __ddiv_rn(w, z);
+    if (E.wout) E.wout[p] = c;
+    const double gr = E.GR[p];
+    const double gi = CPLX ? E.GI[p] : 0.0;
+    const double u = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+    double cc = c;
+    if (!E.squared && c != 0.0) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(u), 1e-150)));
+    const double cr = c == 0.0 ? 0.0 : __dmul_rn(cc, gr);
+    const double ci = c == 0.0 ? 0.0 : __dmul_rn(cc, gi);
+    const double cu = c == 0.0 ? 0.0 : __dmul_rn(cc, u);
+    E.PR[j * N + k] = cr;
+    E.PR[k * N + j] = cr;
+    E.CU[j * N + k] = cu;
+    E.CU[k * N + j] = cu;
+    if (CPLX) {
+      E.PI[j * N + k] = ci;
+      E.PI[k * N + j] = -ci;
+    }
+  }
+}
+
+// ---- K6: chunked gradient GEMM D(q, m) = sum_k phi(q, k) (x) P(k, m)
+// over k in chunk c (ascending), register tile 4 m x RT rows per thread.
+constexpr int GM = 64, GK = 16;
+template <bool CPLX>
+__global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
+  constexpr int RT = CPLX ? 2 : 4;          // complex rows / real rows per thread
+  constexpr int RB = 16 * RT;               // rows per tile (complex rows or real rows)
+  __shared__ double sPr[GK][GM], sPi[GK][GM];
+  __shared__ double sFr[GK][RB], sFi[GK][RB];
+  const int N = E.N, d = E.d, K = E.K;
+  const int mb = blockIdx.x, rb = blockIdx.y, ch = blockIdx.z;
+  const int k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
+  const int tid = threadIdx.x;
+  const int tm = tid & 15, tr = tid >> 4;
+  double ar[RT][4], ai[RT][4];
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) ar[r][c] = ai[r][c] = 0.0;
+  for (int k0 = k_lo; k0 < k_hi; k0 += GK) {
+    __syncthreads();
+    for (int e = tid; e < GK * GM; e += 256) {
+      const int kk = e / GM, c = e - kk * GM;
+      const int k = k0 + kk, m = mb * GM + c;
+      const bool v = k < k_hi && m < N;
+      sPr[kk][c] = v ? E.PR[(long long)k * N + m] : 0.0;
+      if (CPLX) sPi[kk][c] = v ? E.PI[(long long)k * N + m] : 0.0;
+    }
+    for (int e = tid; e < GK * RB; e += 256) {
+      const int kk = e / RB, r = e - kk * RB;
+      const int k = k0 + kk, row = rb * RB + r;
+      const bool v = k < k_hi && row < d;
+      if (CPLX) {
+        sFr[kk][r] = v ? E.phiT[(long long)(2 * row) * N + k] : 0.0;
+        sFi[kk][r] = v ? E.phiT[(long long)(2 * row + 1) * N + k] : 0.0;
+      } else {
+        sFr[kk][r] = v ? E.phiT[(long long)row * N + k] : 0.0;
+      }
+    }
+    __syncthreads();
+    const int kmax = min(GK, k_hi - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      double pr[4], pi[4], fr[RT], fi[RT];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        pr[c] = sPr[kk][tm + 16 * c];
+        if (CPLX) pi[c] = sPi[kk][tm + 16 * c];
+      }
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        fr[r] = sFr[kk][tr + 16 * r];
+        if (CPLX) fi[r] = sFi[kk][tr + 16 * r];
+      }
+#pragma unroll
+      for (int r = 0; r < RT; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (CPLX) {
+            ar[r][c] = fma(fr[r], pr[c], ar[r][c]);
+            ar[r][c] = fma(-fi[r], pi[c], ar[r][c]);
+            ai[r][c] = fma(fr[r], pi[c], ai[r][c]);
+            ai[r][c] = fma(fi[r], pr[c], ai[r][c]);
+          } else {
+            ar[r][c] = fma(fr[r], pr[c], ar[r][c]);
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int row = rb * RB + tr + 16 * r, m = mb * GM + tm + 16 * c;
+      if (row < d && m < N) {
+        double* out = E.part + (long long)ch * E.dim + (long long)m * E.L;
+        if (CPLX) {
+          out[2 * row] = ar[r][c];
+          out[2 * row + 1] = ai[r][c];
+        } else {
+          out[row] = ar[r][c];
+        }
+      }
+    }
+}
+
+// ---- K6b: t chunk partials, thread per (chunk, m), ascending k (c*u add)
+__global__ void large_tsum(LargeEval E) {
+  const int ch = blockIdx.y;
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= E.N) return;
+  const int k_lo = (ch * E.N) / E.K, k_hi = ((ch + 1) * E.N) / E.K;
+  double t = 0.0;
+  for (int k = k_lo; k < k_hi; ++k) t = __dadd_rn(t, E.CU[(long long)k * E.N + m]);
+  E.tpart[(long long)ch * E.N + m] = t;
+}
+
+// ---- K7: chunk partials added left to right; grad = ((acc - t phi)/alpha)*2
+__global__ void large_finalize(LargeEval E) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E.dim) return;
+  const int m = (int)(e / E.L), q = (int)(e - (long long)m * E.L);
+  double a = E.part[e], t = E.tpart[m];
+  for (int ch = 1; ch < E.K; ++ch) {
+    a = __dadd_rn(a, E.part[(long long)ch * E.dim + e]);
+    t = __dadd_rn(t, E.tpart[(long long)ch * E.N + m]);
+  }
+  const double phi = E.phiT[(long long)q * E.N + m];
+  E.gout[e] = __dmul_rn(__ddiv_rn(__dsub_rn(a, __dmul_rn(t, phi)), E.alpha[m]), 2.0);
+}
+
+// ---- vector kernels (trust-region state in HBM)
+// CAS dots of width LS_LANES: up to 3 dots at once, per-CTA tree totals.
+__global__ void __launch_bounds__(LS_THREADS) large_dots(const double* a0, const double* b0, const double* a1,
+                                                          const double* b1, const double* a2, const double* b2, int nd,
+                                                          long long n, double* cta_out) {
+  __shared__ double wt[3][LS_THREADS / 32];
+  const long long t = (long long)blockIdx.x * LS_THREADS + threadIdx.x;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (long long i = t; i < n; i += LS_LANES) {
+    v[0] = fma(a0[i], b0[i], v[0]);
+    if (nd > 1) v[1] = fma(a1[i], b1[i], v[1]);
+    if (nd > 2) v[2] = fma(a2[i], b2[i], v[2]);
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v[q] = __dadd_rn(v[q], __shfl_xor_sync(FULL, v[q], off));
+    if ((threadIdx.x & 31) == 0) wt[q][threadIdx.x >> 5] = v[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double u = threadIdx.x < LS_THREADS / 32 ? wt[q][threadIdx.x] : 0.0;
+#pragma unroll
+      for (int off = 1; off < LS_THREADS / 32; off <<= 1) u = __dadd_rn(u, __shfl_xor_sync(FULL, u, off));
+      if (threadIdx.x == 0) cta_out[q * LS_CTAS + blockIdx.x] = u;
+    }
+  }
+}
+
+__global__ void large_dots_reduce(const double* cta_out, int nd, double* out) {
+  __shared__ double wt[3][LS_CTAS / 32];
+  for (int q = 0; q < nd; ++q) {
+    double v = cta_out[q * LS_CTAS + threadIdx.x];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+    if ((threadIdx.x & 31) == 0) wt[q][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    for (int q = 0; q < nd; ++q) {
+      double u = threadIdx.x < LS_CTAS / 32 ? wt[q][threadIdx.x] : 0.0;
+#pragma unroll
+      for (int off = 1; off < LS_CTAS / 32; off <<= 1) u = __dadd_rn(u, __shfl_xor_sync(FULL, u, off));
+      if (threadIdx.x == 0) out[q] = u;
+    }
+  }
+}
+
+// y = a + s*b elementwise (mul then add)
+__global__ void large_axpy(double* y, const double* a, double s, const double* b, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __dadd_rn(a[i], __dmul_rn(s, b[i]));
+}
+// d = -r + beta*d
+__global__ void large_cg_dir(double* d, const double* r, double beta, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    d[i] = __dadd_rn(-r[i], __dmul_rn(beta, d[i]));
+}
+// hv = (gp - gm) / den
+__global__ void large_fd(double* hv, const double* gp, const double* gm, double den, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    hv[i] = __ddiv_rn(__dsub_rn(gp[i], gm[i]), den);
+}
+__global__ void large_neg(double* y, const double* a, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = -a[i];
+}
+__global__ void large_nonfinite(const double* a, long long n, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) atomicExch(flag, 1);
+}
+
+}  // namespace trstmi_dev

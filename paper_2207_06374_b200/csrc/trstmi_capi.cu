@@ -16,6 +16,7 @@
 #include "batch_kernels.cuh"
 #include "host/host_common.hpp"
 #include "kernel_table.hpp"
+#include "large_engine.hpp"
 
 using namespace trstmi_dev;
 
@@ -72,8 +73,32 @@ struct trstmi_ctx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   int* counter = nullptr;
+  trstmi_large::Engine* large = nullptr;  // large-frame path engine (lazy)
   std::string err;
 };
+
+// ------------------------------------------------------------------ path rule
+static int small_lanes(int field, long long d, long long N) {
+  const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
+  if (dim <= 64) return 32;
+  if (dim <= 256) return 128;
+  return 256;
+}
+
+static bool small_fits(int field, long long d, long long N) {
+  if (d > 16 || N > 4096) return false;
+  const int S = small_lanes(field, d, N);
+  Prob P;
+  P.d = (int)d;
+  P.N = (int)N;
+  P.L = (field == TRSTMI_COMPLEX ? 2 : 1) * (int)d;
+  P.dim = P.L * P.N;
+  P.n = (int)(N * (N - 1) / 2);
+  P.K = kchunks_for(P.d, P.N, S);
+  return anneal_smem_doubles(P, S, field == TRSTMI_COMPLEX) * 8 <= 227LL * 1024;
+}
+
+bool trstmi_large::use_large(int field, long long d, long long N) { return !small_fits(field, d, N); }
 
 namespace {
 
@@ -103,7 +128,7 @@ int check_shape(trstmi_ctx* ctx, int field, long long d, long long N, const char
   if (field != TRSTMI_COMPLEX && field != TRSTMI_REAL) return fail(ctx, TRSTMI_ERR_INVALID_ARG, std::string(who) + ": bad field");
   if (d < 1) return fail(ctx, TRSTMI_ERR_INVALID_ARG, std::string(who) + ": need d >= 1");
   if (N < 2) return fail(ctx, TRSTMI_ERR_INVALID_ARG, std::string(who) + ": need N >= 2");
-  if (d > 16 || N > 4096) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, std::string(who) + ": shape outside the small-frame kernel family (d <= 16)");
+  if (N > 16384 || d > 4096) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, std::string(who) + ": N > 16384 or d > 4096");
   return TRSTMI_OK;
 }
 
@@ -180,12 +205,8 @@ int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t
 int trstmi_kchunks(int field, int64_t d, int64_t N) { return kchunks_for((int)d, (int)N, trstmi_lanes(field, d, N)); }
 
 int trstmi_lanes(int field, int64_t d, int64_t N) {
-  const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
-  const long long n = N * (N - 1) / 2;
-  (void)n;
-  if (dim <= 64) return 32;
-  if (dim <= 256) return 128;
-  return 256;
+  if (trstmi_large::use_large(field, d, N)) return trstmi_large::kLanes;
+  return small_lanes(field, d, N);
 }
 
 void trstmi_cfg_defaults(trstmi_cfg* c, int field, int d, int N) {
@@ -259,12 +280,18 @@ int trstmi_ctx_destroy(trstmi_ctx* ctx) {
   if (!ctx) return TRSTMI_OK;
   cudaSetDevice(ctx->device);
   if (ctx->counter) cudaFree(ctx->counter);
+  if (ctx->large) trstmi_large::engine_destroy(ctx->large);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TRSTMI_OK;
 }
 
 const char* trstmi_last_error(const trstmi_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+static trstmi_large::Engine* large_engine(trstmi_ctx* ctx, cudaStream_t st) {
+  if (!ctx->large) ctx->large = trstmi_large::engine_create(ctx->device, st);
+  return ctx->large;
+}
 
 // ------------------------------------------------------------------ eval / hvp / coherence
 static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t N, BatchArgs& A, cudaStream_t st) {
@@ -291,6 +318,28 @@ int trstmi_eval_batch_dev(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int6
   if (!ctx) return TRSTMI_ERR_INVALID_ARG;
   int rc = check_shape(ctx, field, d, N, "eval_objective");
   if (rc) return rc;
+  cudaSetDevice(ctx->device);
+  if (trstmi_large::use_large(field, d, N)) {
+    const trstmi_large::Shape sh = trstmi_large::make_shape(field, (int)d, (int)N);
+    cudaStream_t st = (cudaStream_t)stream;
+    trstmi_large::Engine* E = large_engine(ctx, st);
+    std::vector<double> hd(B), hF(B), hs(B);
+    std::vector<int64_t> hz(B);
+    CUDA_TRY(ctx, cudaMemcpyAsync(hd.data(), delta, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    for (int64_t b = 0; b < B; ++b) {
+      long long zc;
+      int r2 = trstmi_large::eval(E, sh, pts + b * sh.dim, nullptr, 0.0, hd[b], squared, grad + b * sh.dim, &hF[b],
+                                  &hs[b], weights ? weights + b * sh.n : nullptr, &zc, &ctx->err);
+      if (r2) return r2;
+      hz[b] = zc;
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(F, hF.data(), B * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(s, hs.data(), B * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(zero_col, hz.data(), B * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    return TRSTMI_OK;
+  }
   BatchArgs A{};
   A.P = make_prob(field, d, N);
   A.B = B;
@@ -361,6 +410,22 @@ int trstmi_hvp_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B
   CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, pts, vb, cudaMemcpyHostToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(dr.p, dirs, vb, cudaMemcpyHostToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, delta, B * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (trstmi_large::use_large(field, d, N)) {
+    const trstmi_large::Shape sh = trstmi_large::make_shape(field, (int)d, (int)N);
+    trstmi_large::Engine* E = large_engine(ctx, st);
+    for (int64_t b = 0; b < B; ++b) {
+      int pth;
+      long long zc;
+      int r2 = trstmi_large::hvp(E, sh, (double*)dp.p + b * sh.dim, (double*)dr.p + b * sh.dim, delta[b],
+                                 (double*)dh.p + b * sh.dim, &pth, &zc, &ctx->err);
+      if (r2) return r2;
+      path[b] = pth;
+      zero_col[b] = zc;
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(hv, dh.p, vb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    return TRSTMI_OK;
+  }
   BatchArgs A{};
   A.P = P;
   A.B = B;
@@ -395,6 +460,19 @@ int trstmi_coherence_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int
   CUDA_TRY(ctx, cudaMalloc(&dz.p, B * sizeof(int64_t)));
   cudaStream_t st = ctx->stream;
   CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, frames, vb, cudaMemcpyHostToDevice, st));
+  if (trstmi_large::use_large(field, d, N)) {
+    const trstmi_large::Shape sh = trstmi_large::make_shape(field, (int)d, (int)N);
+    trstmi_large::Engine* E = large_engine(ctx, st);
+    for (int64_t b = 0; b < B; ++b) {
+      long long a, zc;
+      int r2 = trstmi_large::coherence(E, sh, (double*)dp.p + b * sh.dim, normalize, &mu[b], &a, &zc, &ctx->err);
+      if (r2) return r2;
+      argmax_pair[b] = a;
+      zero_col[b] = zc;
+      if (zc >= 0) mu[b] = 0.0;
+    }
+    return TRSTMI_OK;
+  }
   BatchArgs A{};
   A.P = P;
   A.B = B;
@@ -487,6 +565,32 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
   if (rc) return rc;
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (trstmi_large::use_large(cfg->field, cfg->d, cfg->N)) {
+    const trstmi_large::Shape sh = trstmi_large::make_shape(cfg->field, cfg->d, cfg->N);
+    trstmi_large::Engine* E = large_engine(ctx, st);
+    trstmi_large::TrCfg tr{A.tr.delta0, A.tr.delta_max, A.tr.eta, A.tr.shrink, A.tr.grow, A.tr.grad_tol,
+                           A.tr.cg_force_c, A.tr.max_outer, A.tr.max_cg};
+    const int cap = A.record_cap;
+    std::vector<trstmi_trial_out> to(trials);
+    std::vector<trstmi_stage_out> so((size_t)trials * A.n_stages);
+    std::vector<trstmi_outer_out> oo(outer_out_dev && cap ? (size_t)trials * cap : 0);
+    std::memset(so.data(), 0, so.size() * sizeof(trstmi_stage_out));
+    for (int64_t t = 0; t < trials; ++t) {
+      std::memset(&to[t], 0, sizeof(trstmi_trial_out));
+      int r2 = trstmi_large::anneal_trial(E, sh, tr, sched, 0, cap, params_dev + t * sh.dim,
+                                          frames_dev ? frames_dev + t * sh.dim : nullptr,
+                                          rng_state ? rng_state + 3 * t : nullptr, &to[t], so.data() + t * A.n_stages,
+                                          oo.empty() ? nullptr : oo.data() + t * cap, &ctx->err);
+      if (r2) return r2;
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(trial_out_dev, to.data(), trials * sizeof(trstmi_trial_out), cudaMemcpyHostToDevice, st));
+    if (stage_out_dev)
+      CUDA_TRY(ctx, cudaMemcpyAsync(stage_out_dev, so.data(), so.size() * sizeof(trstmi_stage_out), cudaMemcpyHostToDevice, st));
+    if (!oo.empty())
+      CUDA_TRY(ctx, cudaMemcpyAsync(outer_out_dev, oo.data(), oo.size() * sizeof(trstmi_outer_out), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    return TRSTMI_OK;
+  }
   A.n_list = (int)trials;
   A.params = params_dev;
   A.frames = frames_dev;

@@ -1,0 +1,96 @@
+"""GPU parity of the large-frame path (BASELINE configs 4-5 and any shape
+outside the small-frame family): evaluation, Hessian-vector products,
+coherence and anneal trajectories bit-identical to the oracle run with the
+same CAS parameters (S = 32768 lanes, K = 8 gradient chunks)."""
+import numpy as np
+import pytest
+
+from paper_2207_06374_b200 import abi
+from tests import oracle_ffi as orc
+
+pytestmark = pytest.mark.gpu
+
+C, R = abi.COMPLEX, abi.REAL
+LARGE = [(C, 20, 24), (R, 17, 50), (C, 32, 64), (R, 64, 128), (C, 24, 70), (C, 17, 130)]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2207_06374_b200 import api
+    c = api.Context(0)
+    yield c
+    c.close()
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def test_path_rule():
+    from paper_2207_06374_b200 import api
+    assert api.lanes(C, 2, 100) == 256 and api.lanes(C, 6, 36) == 256 and api.lanes(R, 4, 10) == 32
+    for field, d, N in LARGE + [(R, 64, 1024), (C, 128, 4096)]:
+        assert api.lanes(field, d, N) == 32768
+
+
+@pytest.mark.parametrize("field,d,N", LARGE)
+@pytest.mark.parametrize("delta", [1e-1, 1e-4])
+def test_large_eval_bit_exact(ctx, field, d, N, delta):
+    from paper_2207_06374_b200 import api
+    S = api.lanes(field, d, N)
+    pts = np.stack([orc.random_test_frame(field, d, N, s) for s in (5, 6)])
+    pts[1] *= 2.5
+    F, s, g, w, zc = ctx.eval_batch(field, d, N, pts, delta, True, True)
+    for b in range(2):
+        Fo, so, go, wo, zo = orc.eval_objective(field, d, N, S, pts[b], delta, want_weights=True)
+        assert zc[b] == -1 and zo == -1
+        assert bits(F[b]) == bits(Fo) and bits(s[b]) == bits(so)
+        assert np.array_equal(bits(g[b]), bits(go)), np.max(np.abs(g[b] - go))
+        assert np.array_equal(bits(w[b]), bits(wo))
+
+
+@pytest.mark.parametrize("field,d,N", [(R, 64, 1024), (C, 128, 512)])
+def test_config4_scale_eval_bit_exact(ctx, field, d, N):
+    """BASELINE config 4 at full size (real d=64, N=1024) and config 5's d at N=512."""
+    from paper_2207_06374_b200 import api
+    S = api.lanes(field, d, N)
+    x = orc.random_test_frame(field, d, N, 11)
+    for delta in (1e-2, 6e-9):
+        F, s, g, w, zc = ctx.eval_batch(field, d, N, x[None], delta)
+        Fo, so, go, _, zo = orc.eval_objective(field, d, N, S, x, delta)
+        assert bits(F[0]) == bits(Fo)
+        assert np.array_equal(bits(g[0]), bits(go))
+
+
+@pytest.mark.parametrize("field,d,N", LARGE[:4])
+def test_large_hvp_and_coherence_bit_exact(ctx, field, d, N):
+    from paper_2207_06374_b200 import api
+    S = api.lanes(field, d, N)
+    x = orc.random_test_frame(field, d, N, 3)
+    rng = np.random.default_rng(d + N)
+    dirs = rng.standard_normal(x.size)
+    hv, path, zc = ctx.hvp_batch(field, d, N, x[None], dirs[None], 1e-3)
+    ho, po, zo = orc.hvp(field, d, N, S, x, dirs, 1e-3)
+    assert path[0] == po == abi.HVP_CENTRAL
+    assert np.array_equal(bits(hv[0]), bits(ho))
+    for normalize in (False, True):
+        mu, arg, z2 = ctx.coherence_batch(field, d, N, (x * 1.7)[None], normalize)
+        mo, ao, _ = orc.coherence(field, d, N, x * 1.7, normalize)
+        assert bits(mu[0]) == bits(mo) and arg[0] == ao
+
+
+@pytest.mark.parametrize("field,d,N,trials,max_outer", [(C, 20, 24, 2, 6), (R, 17, 40, 2, 5)])
+def test_large_anneal_trajectory_bit_exact(ctx, field, d, N, trials, max_outer):
+    from paper_2207_06374_b200 import api
+    from tests.test_gpu_parity import _cmp_solve
+    cfg = abi.default_cfg(field, d, N, max_outer)
+    cfg.n_stages = 3
+    sched = api.default_schedule(N)
+    for k in range(3):
+        cfg.schedule[k] = sched[k]
+    cfg.record_cap = 400
+    S = api.lanes(field, d, N)
+    starts, st = api.random_frames(field, d, N, 0, 0, trials)
+    g = ctx.solve_batch(cfg, starts, st)
+    o = orc.solve_batch(cfg, S, starts, st, threads=2)
+    _cmp_solve(g, o, trials, 3, 400)
