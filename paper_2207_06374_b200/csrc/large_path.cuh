@@ -382,6 +382,7 @@ __global__ void large_tsum(LargeEval E) {
   if (m >= E.N) return;
   const int k_lo = (ch * E.N) / E.K, k_hi = ((ch + 1) * E.N) / E.K;
   double t = 0.0;
+#pragma unroll 16
   for (int k = k_lo; k < k_hi; ++k) t = __dadd_rn(t, E.CU[(long long)k * E.N + m]);
   E.tpart[(long long)ch * E.N + m] = t;
 }

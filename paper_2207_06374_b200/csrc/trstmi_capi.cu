@@ -8,7 +8,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -74,6 +76,7 @@ struct trstmi_ctx {
   cudaStream_t stream = nullptr;
   int* counter = nullptr;
   trstmi_large::Engine* large = nullptr;  // large-frame path engine (lazy)
+  int large_workers = 8;                  // concurrent large-path trials (streams)
   std::string err;
 };
 
@@ -567,7 +570,6 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
   cudaStream_t st = (cudaStream_t)stream;
   if (trstmi_large::use_large(cfg->field, cfg->d, cfg->N)) {
     const trstmi_large::Shape sh = trstmi_large::make_shape(cfg->field, cfg->d, cfg->N);
-    trstmi_large::Engine* E = large_engine(ctx, st);
     trstmi_large::TrCfg tr{A.tr.delta0, A.tr.delta_max, A.tr.eta, A.tr.shrink, A.tr.grow, A.tr.grad_tol,
                            A.tr.cg_force_c, A.tr.max_outer, A.tr.max_cg};
     const int cap = A.record_cap;
@@ -575,14 +577,39 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
     std::vector<trstmi_stage_out> so((size_t)trials * A.n_stages);
     std::vector<trstmi_outer_out> oo(outer_out_dev && cap ? (size_t)trials * cap : 0);
     std::memset(so.data(), 0, so.size() * sizeof(trstmi_stage_out));
-    for (int64_t t = 0; t < trials; ++t) {
-      std::memset(&to[t], 0, sizeof(trstmi_trial_out));
-      int r2 = trstmi_large::anneal_trial(E, sh, tr, sched, 0, cap, params_dev + t * sh.dim,
-                                          frames_dev ? frames_dev + t * sh.dim : nullptr,
-                                          rng_state ? rng_state + 3 * t : nullptr, &to[t], so.data() + t * A.n_stages,
-                                          oo.empty() ? nullptr : oo.data() + t * cap, &ctx->err);
-      if (r2) return r2;
+    // Trial scheduler (the reference's restart thread pool, solver.hpp:239-254):
+    // host workers, one CUDA stream + engine each, pull trial ids from an
+    // atomic counter; each drives its trial's trust-region loop.
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    const int workers = (int)std::max<int64_t>(1, std::min<int64_t>(trials, ctx->large_workers));
+    std::atomic<int64_t> next{0};
+    std::vector<int> rcs(workers, TRSTMI_OK);
+    std::vector<std::string> errs(workers);
+    auto work = [&](int wi) {
+      cudaSetDevice(ctx->device);
+      cudaStream_t ws = nullptr;
+      cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking);
+      trstmi_large::Engine* E = trstmi_large::engine_create(ctx->device, ws);
+      for (int64_t t = next.fetch_add(1); t < trials && rcs[wi] == TRSTMI_OK; t = next.fetch_add(1)) {
+        std::memset(&to[t], 0, sizeof(trstmi_trial_out));
+        rcs[wi] = trstmi_large::anneal_trial(E, sh, tr, sched, 0, cap, params_dev + t * sh.dim,
+                                             frames_dev ? frames_dev + t * sh.dim : nullptr,
+                                             rng_state ? rng_state + 3 * t : nullptr, &to[t],
+                                             so.data() + t * A.n_stages, oo.empty() ? nullptr : oo.data() + t * cap,
+                                             &errs[wi]);
+      }
+      trstmi_large::engine_destroy(E);
+      cudaStreamDestroy(ws);
+    };
+    if (workers == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (int wi = 0; wi < workers; ++wi) pool.emplace_back(work, wi);
+      for (auto& th : pool) th.join();
     }
+    for (int wi = 0; wi < workers; ++wi)
+      if (rcs[wi]) return fail(ctx, rcs[wi], errs[wi]);
     CUDA_TRY(ctx, cudaMemcpyAsync(trial_out_dev, to.data(), trials * sizeof(trstmi_trial_out), cudaMemcpyHostToDevice, st));
     if (stage_out_dev)
       CUDA_TRY(ctx, cudaMemcpyAsync(stage_out_dev, so.data(), so.size() * sizeof(trstmi_stage_out), cudaMemcpyHostToDevice, st));
