@@ -224,6 +224,7 @@ struct Shape {
   std::int64_t d = 0, N = 0;
   int lanes = 32;             // CAS reduction width S (trstmi_lanes())
   int kchunks = 1;            // CAS gradient k-chunks K (trstmi_kchunks())
+  int zrows = 0;              // large path: z over row blocks of zrows rows (0: one lane-strided sum)
   std::int64_t comps() const { return complex_field ? 2 : 1; }
   std::int64_t col_len() const { return comps() * d; }  // doubles per column
   std::int64_t dim() const { return col_len() * N; }
@@ -311,7 +312,22 @@ inline EvalResult eval_objective(const Shape& sh, const double* x, const double*
     const double diff = xv[p] - s;
     w[p] = (diff < cut) ? 0.0 : cas_exp(diff / delta);
   }
-  const double z = cas_sum(w.data(), n, sh.lanes);
+  // z (smoothing.hpp:121-124) in the CAS order: small path — one lane-strided
+  // sum of width S over all pairs; large path — the pairs of each block of
+  // zrows consecutive rows (a contiguous pair range) summed with 256 lanes,
+  // block sums added in row order (so any row-block sharding is exact).
+  double z;
+  if (sh.zrows > 0) {
+    z = 0.0;
+    for (std::int64_t r0 = 0, b = 0; r0 < N; r0 += sh.zrows, ++b) {
+      const std::int64_t r1 = std::min<std::int64_t>(N, r0 + sh.zrows);
+      const std::int64_t p0 = r0 * N - r0 * (r0 + 1) / 2, p1 = r1 * N - r1 * (r1 + 1) / 2;
+      const double zb = cas_sum(w.data() + p0, p1 - p0, 256);
+      z = (b == 0) ? zb : z + zb;
+    }
+  } else {
+    z = cas_sum(w.data(), n, sh.lanes);
+  }
   for (std::int64_t p = 0; p < n; ++p) w[p] = w[p] / z;
   out.s = s;
   out.value = s + delta * cas_log(z);

@@ -28,6 +28,7 @@ Shape make_shape(int field, std::int64_t d, std::int64_t N, int lanes) {
   sh.N = N;
   sh.lanes = lanes;
   sh.kchunks = kchunks_for(d, N, lanes);
+  sh.zrows = (lanes == 32768) ? 16 : 0;  // large-frame path (trstmi_lanes == 32768)
   return sh;
 }
 

@@ -113,7 +113,7 @@ static int ensure(Engine* E, const Shape& sh, std::string* err) {
   LCHK(cudaMalloc(&w.X, (size_t)std::max<long long>(sh.n, 1) * 8));
   LCHK(cudaMalloc(&w.GR, (size_t)std::max<long long>(sh.n, 1) * 8));
   LCHK(cudaMalloc(&w.GI, sh.cplx ? (size_t)std::max<long long>(sh.n, 1) * 8 : 8));
-  LCHK(cudaMalloc(&w.zpart, LS_CTAS * 8));
+  LCHK(cudaMalloc(&w.zpart, (size_t)((sh.N + ZROWS - 1) / ZROWS) * 8));
   LCHK(cudaMalloc(&w.scal, 8 * 8));
   LCHK(cudaMalloc(&w.PR, N2 * 8));
   LCHK(cudaMalloc(&w.PI, sh.cplx ? N2 * 8 : 8));
@@ -182,8 +182,9 @@ int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double 
   const int tiles = nt * (nt + 1) / 2;
   if (sh.cplx) large_gram<true, 0><<<tiles, 256, 0, st>>>(L, nullptr, nullptr);
   else large_gram<false, 0><<<tiles, 256, 0, st>>>(L, nullptr, nullptr);
-  large_weights<<<LS_CTAS, LS_THREADS, 0, st>>>(L);
-  large_zreduce<<<1, LS_CTAS, 0, st>>>(L);
+  const int nzb = (sh.N + ZROWS - 1) / ZROWS;
+  large_weights<<<nzb, ZLANES, 0, st>>>(L);
+  large_zreduce<<<1, 32, 0, st>>>(L, nzb);
   const int cblocks = (int)std::min<long long>((sh.n + 255) / 256, 148LL * 16);
   if (sh.cplx) large_coef<true><<<std::max(cblocks, 1), 256, 0, st>>>(L);
   else large_coef<false><<<std::max(cblocks, 1), 256, 0, st>>>(L);

@@ -5,16 +5,18 @@
 //   K1 large_normalize   alpha_j, phi = p/alpha (component-major), first zero column
 //   K2 large_gram        upper-triangular 64x64 register-tiled Gram (SYRK) ->
 //                        x_p, G(j,k) packed; s = max x_p (atomicMax on the bits)
-//   K3 large_weights     w_p = exp((x_p - s)/delta); lane partials of z
-//   K4 large_zreduce     z (CAS tree over the 128 CTA totals); F = s + delta log z
+//   K3 large_weights     w_p = exp((x_p - s)/delta); z partial per 16-row block
+//   K4 large_zreduce     z = block partials in row order; F = s + delta log z
 //   K5 large_coef        c = w/z; dense coefficient matrices P = c G (k,m) and c u
 //   K6 large_grad_gemm   chunked D = Phi P (register-tiled DGEMM, CAS k-chunks)
 //   K6b large_tsum       t chunk partials
 //   K7 large_finalize    chunk combine, grad = ((acc - t phi)/alpha) * 2
 //
 // Arithmetic is the Canonical Arithmetic Spec with S = 32768
-// reduction lanes (128 CTAs x 256 threads) and K = clamp(S/N, 1, 8) gradient
-// chunks, so every value is bit-identical to the oracle run with the same S.
+// reduction lanes for dots (128 CTAs x 256 threads), z summed per 16-row block
+// (so a row-block sharding across GPUs reproduces it exactly) and
+// K = clamp(S/N, 1, 8) gradient chunks: every value is bit-identical to the
+// oracle run with the same parameters.
 // FP64 tensor cores are not used: sm_100a has no FP64 tcgen05 kind, and the
 // legacy DMMA peak equals the DFMA peak on B200 while its internal summation
 // order is unspecified — SIMT DFMA tiles keep the CAS order exact.
@@ -210,14 +212,19 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
   }
 }
 
-// ---- K3: weights and CAS lane partials of z (lane t = global thread id)
-__global__ void __launch_bounds__(LS_THREADS) large_weights(LargeEval E) {
-  __shared__ double wt[LS_THREADS / 32];
+// ---- K3: weights; z partial of each block of ZROWS rows (one CTA per block,
+// 256 CAS lanes over the block's contiguous pair range)
+constexpr int ZROWS = 16;
+constexpr int ZLANES = 256;
+__global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
+  __shared__ double wt[ZLANES / 32];
   const double s = __longlong_as_double((long long)*E.smax_bits);
   const double cut = __dmul_rn(kUnderflowCut, E.delta);
-  const long long t = (long long)blockIdx.x * LS_THREADS + threadIdx.x;
+  const long long N = E.N;
+  const long long r0 = (long long)blockIdx.x * ZROWS, r1 = min(N, r0 + ZROWS);
+  const long long p0 = r0 * N - r0 * (r0 + 1) / 2, p1 = r1 * N - r1 * (r1 + 1) / 2;
   double zp = 0.0;
-  for (long long p = t; p < E.n; p += LS_LANES) {
+  for (long long p = p0 + threadIdx.x; p < p1; p += ZLANES) {
     const double diff = __dsub_rn(E.X[p], s);
     const double w = (diff < cut) ? 0.0 : cas_exp(__ddiv_rn(diff, E.delta));
     E.X[p] = w;
@@ -228,31 +235,21 @@ __global__ void __launch_bounds__(LS_THREADS) large_weights(LargeEval E) {
   if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = zp;
   __syncthreads();
   if (threadIdx.x < 32) {
-    double v = threadIdx.x < LS_THREADS / 32 ? wt[threadIdx.x] : 0.0;
+    double v = threadIdx.x < ZLANES / 32 ? wt[threadIdx.x] : 0.0;
 #pragma unroll
-    for (int off = 1; off < LS_THREADS / 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+    for (int off = 1; off < ZLANES / 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
     if (threadIdx.x == 0) E.zpart[blockIdx.x] = v;
     if (blockIdx.x == 0 && threadIdx.x == 0) E.scal[0] = s;
   }
 }
 
-// ---- K4: z = pairwise tree over the CTA totals (continuing the warp tree)
-__global__ void large_zreduce(LargeEval E) {
-  __shared__ double wt[LS_CTAS / 32];
-  double v = E.zpart[threadIdx.x];
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
-  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double u = threadIdx.x < LS_CTAS / 32 ? wt[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int off = 1; off < LS_CTAS / 32; off <<= 1) u = __dadd_rn(u, __shfl_xor_sync(FULL, u, off));
-    if (threadIdx.x == 0) {
-      E.scal[1] = u;
-      E.scal[2] = __dadd_rn(E.scal[0], __dmul_rn(E.delta, cas_log(u)));
-    }
-  }
+// ---- K4: z = block sums added in row order; F = s + delta log z
+__global__ void large_zreduce(LargeEval E, int nblocks) {
+  if (threadIdx.x != 0) return;
+  double z = E.zpart[0];
+  for (int b = 1; b < nblocks; ++b) z = __dadd_rn(z, E.zpart[b]);
+  E.scal[1] = z;
+  E.scal[2] = __dadd_rn(E.scal[0], __dmul_rn(E.delta, cas_log(z)));
 }
 
 // ---- K5: coefficients into dense P (row k, column m): P(k,m) = c G(k,m)
