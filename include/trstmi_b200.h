@@ -158,6 +158,16 @@ int trstmi_measure_dfma_peak(trstmi_ctx* ctx, int iters, double* tflops);
 int trstmi_selftest_cas_math(trstmi_ctx* ctx, int which, const double* x, double* y, int64_t n);
 int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t* mismatches);
 
+/* ---- single-frame row-block sharding (large-frame path) ----
+ * The frame's Gram rows are split into 64-row blocks over `world` ranks; each
+ * rank computes the tiles touching its rows, its z-block partials and its
+ * gradient columns; the exchanges (max s, z partials, gradient slices) are
+ * NCCL collectives.  Results are bit-identical for every world size.
+ * nccl_id == NULL with world > 1 runs `world` virtual ranks on this device
+ * (each with its own workspace) — the single-GPU test of the partitioning. */
+int trstmi_nccl_unique_id(char* out128);
+int trstmi_set_shard(trstmi_ctx* ctx, int world, int rank, const char* nccl_id);
+
 /* CAS reduction width S used for a shape: the lane count of
  * every dot / norm / z-sum.  The oracle takes the same S. */
 int trstmi_lanes(int field, int64_t d, int64_t N);

@@ -73,6 +73,8 @@ def load_library():
     lib.trstmi_solve_batch.argtypes = [vp, vp, c_i64, vp, vp, vp, vp, vp, vp]
     lib.trstmi_solve_batch_dev.argtypes = [vp, vp, c_i64, vp, vp, vp, vp, vp, vp, vp]
     lib.trstmi_solve.argtypes = [vp, vp, c_i64, ctypes.c_uint64, c_i64, vp, vp, vp, vp, vp]
+    lib.trstmi_nccl_unique_id.argtypes = [vp]
+    lib.trstmi_set_shard.argtypes = [vp, c_int, c_int, vp]
     _lib = lib
     return lib
 
@@ -119,6 +121,14 @@ class Context:
         if rc == abi.TRSTMI_ERR_UNSUPPORTED:
             raise UnsupportedShapeError(msg)
         raise CudaError("%s: %s (code %d)" % (who, msg, rc))
+
+    def set_shard(self, world, rank=0, nccl_id=None):
+        """Row-block sharding of single large frames over `world` ranks
+        (trstmi_set_shard); nccl_id None -> virtual ranks on this device."""
+        buf = None
+        if nccl_id is not None:
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self.check(self.lib.trstmi_set_shard(self.h, world, rank, buf), "set_shard")
 
     # ---------------------------------------------------------------- objective
     def eval_batch(self, field, d, N, pts, delta, squared=True, want_weights=False):
@@ -180,6 +190,15 @@ class Context:
                                          ctypes.cast(oo, ctypes.c_void_p) if oo is not None else None)
         self.check(rc, "solve_batch")
         return dict(params=params, frames=frames, trials=to, stages=so, outer=oo, n_stages=ns, rng=rng)
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId (rank 0 creates it and shares it with the others)."""
+    buf = ctypes.create_string_buffer(128)
+    rc = load_library().trstmi_nccl_unique_id(buf)
+    if rc:
+        raise CudaError("ncclGetUniqueId failed (%d)" % rc)
+    return buf.raw
 
 
 def default_schedule(N, eps_target=1e-7):

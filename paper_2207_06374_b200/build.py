@@ -72,7 +72,7 @@ def build(verbose=False, force=False, jobs=None):
             if verbose and log.strip():
                 print(log)
     tmp = LIB + ".tmp"
-    _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"])
+    _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static", "-lnccl"])
     os.replace(tmp, LIB)
     build_host_tests()
     return LIB

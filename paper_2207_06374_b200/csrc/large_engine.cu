@@ -7,6 +7,8 @@
 #include <limits>
 #include <map>
 
+#include <nccl.h>
+
 #include "host/host_common.hpp"
 #include "large_path.cuh"
 
@@ -36,6 +38,14 @@ struct Engine {
   int device = 0;
   cudaStream_t st = nullptr;
   Work w;
+  // single-frame row-block sharding: world ranks; virtual ranks
+  // run every rank's share on this device in sequence (each with its own
+  // workspace, exchanges by device copies); otherwise one rank per process
+  // with NCCL collectives on st.
+  int world = 1, rank = 0;
+  bool virtual_ranks = false;
+  ncclComm_t nccl = nullptr;
+  std::vector<Work> vw;
   double* dots_cta = nullptr;
   double* dots_out = nullptr;
   int* flag = nullptr;
@@ -94,6 +104,8 @@ static void free_work(Work& w) {
 void engine_destroy(Engine* E) {
   if (!E) return;
   free_work(E->w);
+  for (Work& w : E->vw) free_work(w);
+  if (E->nccl) ncclCommDestroy(E->nccl);
   cudaFree(E->dots_cta);
   cudaFree(E->dots_out);
   cudaFree(E->flag);
@@ -101,8 +113,7 @@ void engine_destroy(Engine* E) {
   delete E;
 }
 
-static int ensure(Engine* E, const Shape& sh, std::string* err) {
-  Work& w = E->w;
+static int alloc_work(Work& w, const Shape& sh, std::string* err) {
   if (w.valid && w.sh.cplx == sh.cplx && w.sh.d == sh.d && w.sh.N == sh.N) return TRSTMI_OK;
   free_work(w);
   const size_t N2 = (size_t)sh.N * sh.N;
@@ -114,6 +125,7 @@ static int ensure(Engine* E, const Shape& sh, std::string* err) {
   LCHK(cudaMalloc(&w.GR, (size_t)std::max<long long>(sh.n, 1) * 8));
   LCHK(cudaMalloc(&w.GI, sh.cplx ? (size_t)std::max<long long>(sh.n, 1) * 8 : 8));
   LCHK(cudaMalloc(&w.zpart, (size_t)((sh.N + ZROWS - 1) / ZROWS) * 8));
+  LCHK(cudaMemset(w.zpart, 0, (size_t)((sh.N + ZROWS - 1) / ZROWS) * 8));
   LCHK(cudaMalloc(&w.scal, 8 * 8));
   LCHK(cudaMalloc(&w.PR, N2 * 8));
   LCHK(cudaMalloc(&w.PI, sh.cplx ? N2 * 8 : 8));
@@ -134,9 +146,10 @@ static int ensure(Engine* E, const Shape& sh, std::string* err) {
   return TRSTMI_OK;
 }
 
-static LargeEval make_eval(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta,
-                           int squared, double* grad, double* weights) {
-  Work& w = E->w;
+static int ensure(Engine* E, const Shape& sh, std::string* err) { return alloc_work(E->w, sh, err); }
+
+static LargeEval make_eval_w(Work& w, const Shape& sh, const double* x, const double* dir, double sc, double delta,
+                             int squared, double* grad, double* weights) {
   LargeEval L;
   L.cplx = sh.cplx;
   L.d = sh.d;
@@ -166,11 +179,22 @@ static LargeEval make_eval(Engine* E, const Shape& sh, const double* x, const do
   L.tpart = w.tpart;
   L.gout = grad;
   L.wout = weights;
+  L.m0 = 0;
+  L.m1 = sh.N;
   return L;
 }
 
+static LargeEval make_eval(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta,
+                           int squared, double* grad, double* weights) {
+  return make_eval_w(E->w, sh, x, dir, sc, delta, squared, grad, weights);
+}
+
+static int eval_sharded(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta,
+                        int squared, double* grad, double* F, double* s, long long* zero_col, std::string* err);
+
 int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta, int squared,
          double* grad, double* F, double* s, double* weights, long long* zero_col, std::string* err) {
+  if (E->world > 1 && !weights) return eval_sharded(E, sh, x, dir, sc, delta, squared, grad, F, s, zero_col, err);
   int rc = ensure(E, sh, err);
   if (rc) return rc;
   Work& w = E->w;
@@ -211,6 +235,172 @@ int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double 
   *zero_col = -1;
   *s = E->h_scal[0];
   *F = E->h_scal[2];
+  return TRSTMI_OK;
+}
+
+#define NCHK(expr)                                                        \
+  do {                                                                    \
+    ncclResult_t r_ = (expr);                                             \
+    if (r_ != ncclSuccess) {                                              \
+      if (err) *err = std::string(#expr ": ") + ncclGetErrorString(r_);   \
+      return TRSTMI_ERR_NCCL;                                             \
+    }                                                                     \
+  } while (0)
+
+// Rank r of `world` owns the 64-row blocks [r*NB/world, (r+1)*NB/world).
+static void shard_rows(const Shape& sh, int world, int r, int* m0, int* m1) {
+  const int NB = (sh.N + GT - 1) / GT;
+  *m0 = std::min(sh.N, GT * (int)((long long)r * NB / world));
+  *m1 = std::min(sh.N, GT * (int)((long long)(r + 1) * NB / world));
+}
+
+// One evaluation with the frame's Gram rows sharded over E->world ranks:
+// each rank computes the Gram tiles touching its rows/columns, its 16-row z
+// blocks and the gradient columns it owns; exchanges are a max of s, the
+// z-block partials and the gradient column slices (all pure data movement, so
+// the result is bit-identical for every world size).
+static int eval_sharded(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta,
+                        int squared, double* grad, double* F, double* s, long long* zero_col, std::string* err) {
+  int rc = ensure(E, sh, err);
+  if (rc) return rc;
+  cudaStream_t st = E->st;
+  const int G = E->world;
+  std::vector<int> ranks;
+  if (E->virtual_ranks) {
+    if ((int)E->vw.size() != G) E->vw.resize(G);
+    for (int r = 0; r < G; ++r) {
+      if ((rc = alloc_work(E->vw[r], sh, err))) return rc;
+      ranks.push_back(r);
+    }
+  } else {
+    ranks.push_back(E->rank);
+  }
+  auto work = [&](int r) -> Work& { return E->virtual_ranks ? E->vw[r] : E->w; };
+  std::vector<LargeEval> Ls(G);
+  for (int r : ranks) {
+    LargeEval L = make_eval_w(work(r), sh, x, dir, sc, delta, squared, grad, nullptr);
+    shard_rows(sh, G, r, &L.m0, &L.m1);
+    Ls[r] = L;
+  }
+  const int nt = (sh.N + GT - 1) / GT;
+  const int tiles = nt * (nt + 1) / 2;
+  const int nzb = (sh.N + ZROWS - 1) / ZROWS;
+  // phase A: normalise, Gram of the shard's tiles, local max
+  for (int r : ranks) {
+    LCHK(cudaMemsetAsync(work(r).zero_col, 0x7f, 4, st));
+    large_normalize<<<(sh.N + 127) / 128, 128, 0, st>>>(Ls[r]);
+    if (sh.cplx) large_gram<true, 0><<<tiles, 256, 0, st>>>(Ls[r], nullptr, nullptr);
+    else large_gram<false, 0><<<tiles, 256, 0, st>>>(Ls[r], nullptr, nullptr);
+  }
+  LCHK(cudaGetLastError());
+  // exchange: s = max over ranks (x >= 0, so the bit patterns order like the values)
+  if (E->virtual_ranks) {
+    unsigned long long mx = 0, v = 0;
+    for (int r : ranks) {
+      LCHK(cudaMemcpyAsync(&v, work(r).smax, 8, cudaMemcpyDeviceToHost, st));
+      LCHK(cudaStreamSynchronize(st));
+      mx = std::max(mx, v);
+    }
+    for (int r : ranks) LCHK(cudaMemcpyAsync(work(r).smax, &mx, 8, cudaMemcpyHostToDevice, st));
+    LCHK(cudaStreamSynchronize(st));
+  } else {
+    NCHK(ncclAllReduce(E->w.smax, E->w.smax, 1, ncclUint64, ncclMax, E->nccl, st));
+  }
+  // phase B: weights of the shard's pairs, z partials of its 16-row blocks
+  for (int r : ranks) large_weights<<<nzb, ZLANES, 0, st>>>(Ls[r]);
+  LCHK(cudaGetLastError());
+  // exchange: every rank's z-block partials to every rank
+  auto zslice = [&](int r, int* b0, int* cnt) {
+    int m0, m1;
+    shard_rows(sh, G, r, &m0, &m1);
+    *b0 = m0 / ZROWS;
+    *cnt = (m1 + ZROWS - 1) / ZROWS - *b0;
+  };
+  if (E->virtual_ranks) {
+    for (int r : ranks) {
+      int b0, cnt;
+      zslice(r, &b0, &cnt);
+      for (int q : ranks)
+        if (q != r && cnt > 0)
+          LCHK(cudaMemcpyAsync(work(q).zpart + b0, work(r).zpart + b0, (size_t)cnt * 8, cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    NCHK(ncclGroupStart());
+    for (int r = 0; r < G; ++r) {
+      int b0, cnt;
+      zslice(r, &b0, &cnt);
+      if (cnt > 0) NCHK(ncclBroadcast(E->w.zpart + b0, E->w.zpart + b0, (size_t)cnt, ncclDouble, r, E->nccl, st));
+    }
+    NCHK(ncclGroupEnd());
+  }
+  // phase C: z, coefficients, gradient columns of the shard
+  const int RB = sh.cplx ? 32 : 64;
+  for (int r : ranks) {
+    const LargeEval& L = Ls[r];
+    large_zreduce<<<1, 32, 0, st>>>(L, nzb);
+    const int cblocks = (int)std::min<long long>((sh.n + 255) / 256, 148LL * 16);
+    if (sh.cplx) large_coef<true><<<std::max(cblocks, 1), 256, 0, st>>>(L);
+    else large_coef<false><<<std::max(cblocks, 1), 256, 0, st>>>(L);
+    const int cols = L.m1 - L.m0;
+    if (cols > 0) {
+      dim3 gg((cols + GM - 1) / GM, (sh.d + RB - 1) / RB, sh.K);
+      if (sh.cplx) large_grad_gemm<true><<<gg, 256, 0, st>>>(L);
+      else large_grad_gemm<false><<<gg, 256, 0, st>>>(L);
+      large_tsum<<<dim3((cols + 127) / 128, sh.K), 128, 0, st>>>(L);
+      large_finalize<<<(int)(((long long)cols * sh.L + 255) / 256), 256, 0, st>>>(L);
+    }
+  }
+  LCHK(cudaGetLastError());
+  if (!E->virtual_ranks) {  // gradient column slices to every rank
+    NCHK(ncclGroupStart());
+    for (int r = 0; r < G; ++r) {
+      int m0, m1;
+      shard_rows(sh, G, r, &m0, &m1);
+      const size_t cnt = (size_t)(m1 - m0) * sh.L;
+      if (cnt) NCHK(ncclBroadcast(grad + (size_t)m0 * sh.L, grad + (size_t)m0 * sh.L, cnt, ncclDouble, r, E->nccl, st));
+    }
+    NCHK(ncclGroupEnd());
+  }
+  Work& w0 = work(ranks[0]);
+  LCHK(cudaMemcpyAsync(E->h_scal, w0.scal, 3 * 8, cudaMemcpyDeviceToHost, st));
+  LCHK(cudaMemcpyAsync(E->h_scal + 4, w0.zero_col, 4, cudaMemcpyDeviceToHost, st));
+  LCHK(cudaStreamSynchronize(st));
+  int zc;
+  std::memcpy(&zc, E->h_scal + 4, 4);
+  if (zc >= 0 && zc < sh.N) {
+    LCHK(cudaMemsetAsync(grad, 0, (size_t)sh.dim * 8, st));
+    *zero_col = zc;
+    *F = std::numeric_limits<double>::infinity();
+    *s = 0.0;
+    return TRSTMI_OK;
+  }
+  *zero_col = -1;
+  *s = E->h_scal[0];
+  *F = E->h_scal[2];
+  return TRSTMI_OK;
+}
+
+int engine_set_shard(Engine* E, int world, int rank, const void* nccl_id, std::string* err) {
+  if (E->nccl) {
+    ncclCommDestroy(E->nccl);
+    E->nccl = nullptr;
+  }
+  E->world = world < 1 ? 1 : world;
+  E->rank = rank;
+  E->virtual_ranks = nccl_id == nullptr && world > 1;
+  if (!E->virtual_ranks && world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    cudaSetDevice(E->device);
+    NCHK(ncclCommInitRank(&E->nccl, world, id, rank));
+  }
+  return TRSTMI_OK;
+}
+
+int nccl_unique_id(void* out, std::string* err) {
+  ncclUniqueId id;
+  NCHK(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
   return TRSTMI_OK;
 }
 

@@ -32,6 +32,12 @@ struct Engine;
 Engine* engine_create(int device, cudaStream_t stream);
 void engine_destroy(Engine*);
 
+// Row-block sharding of a single frame over `world` ranks.
+// nccl_id == NULL: virtual ranks, all shares computed on this device (tests);
+// else this process is `rank` of a NCCL communicator (128-byte ncclUniqueId).
+int engine_set_shard(Engine* E, int world, int rank, const void* nccl_id, std::string* err);
+int nccl_unique_id(void* out128, std::string* err);
+
 // All pointers are device pointers.  Returns TRSTMI_* status; *zero_col = -1
 // or the first zero column (then *F = +inf and grad = 0).
 int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta, int squared,

@@ -56,6 +56,7 @@ struct LargeEval {
   double* tpart;                   // K x N
   double* gout;                    // dim
   double* wout;                    // n or null
+  int m0, m1;                      // owned rows / gradient columns [m0, m1) (row-block shard; full = [0, N))
 };
 
 // ---- K1
@@ -105,6 +106,10 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
   const int nt = (N + GT - 1) / GT;
   int jb, kb;
   tile_of(blockIdx.x, nt, jb, kb);
+  if (MODE == 0) {  // shard: tiles touching the owned rows (as row block) or columns (as column block)
+    const int b0 = E.m0 / GT, b1 = (E.m1 + GT - 1) / GT;
+    if (!((jb >= b0 && jb < b1) || (kb >= b0 && kb < b1))) return;
+  }
   const int tid = threadIdx.x;
   const int tj = tid >> 4, tk = tid & 15;  // 16 x 16 threads, each 4 j x 4 k (strided by 16)
   double re[4][4], im[4][4];
@@ -222,6 +227,18 @@ __global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
   const double cut = __dmul_rn(kUnderflowCut, E.delta);
   const long long N = E.N;
   const long long r0 = (long long)blockIdx.x * ZROWS, r1 = min(N, r0 + ZROWS);
+  if (r0 >= E.m1) return;
+  if (r0 < E.m0) {  // rows before the shard: only the pairs in owned columns (no z)
+    for (long long r = r0; r < r1; ++r) {
+      const long long base = r * N - r * (r + 1) / 2 - r - 1;
+      for (long long k = max(r + 1, (long long)E.m0) + threadIdx.x; k < E.m1; k += ZLANES) {
+        const long long p = base + k;
+        const double diff = __dsub_rn(E.X[p], s);
+        E.X[p] = (diff < cut) ? 0.0 : cas_exp(__ddiv_rn(diff, E.delta));
+      }
+    }
+    return;
+  }
   const long long p0 = r0 * N - r0 * (r0 + 1) / 2, p1 = r1 * N - r1 * (r1 + 1) / 2;
   double zp = 0.0;
   for (long long p = p0 + threadIdx.x; p < p1; p += ZLANES) {
@@ -239,13 +256,14 @@ __global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
 #pragma unroll
     for (int off = 1; off < ZLANES / 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
     if (threadIdx.x == 0) E.zpart[blockIdx.x] = v;
-    if (blockIdx.x == 0 && threadIdx.x == 0) E.scal[0] = s;
   }
+  if (threadIdx.x == 0 && r0 == E.m0) E.scal[0] = s;
 }
 
 // ---- K4: z = block sums added in row order; F = s + delta log z
 __global__ void large_zreduce(LargeEval E, int nblocks) {
   if (threadIdx.x != 0) return;
+  E.scal[0] = __longlong_as_double((long long)*E.smax_bits);
   double z = E.zpart[0];
   for (int b = 1; b < nblocks; ++b) z = __dadd_rn(z, E.zpart[b]);
   E.scal[1] = z;
@@ -257,7 +275,8 @@ template <bool CPLX>
 __global__ void large_coef(LargeEval E) {
   const double z = E.scal[1];
   const int N = E.N;
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < E.n; p += (long long)gridDim.x * blockDim.x) {
+  const long long pend = (long long)E.m1 * N - (long long)E.m1 * (E.m1 + 1) / 2;  // rows < m1
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pend; p += (long long)gridDim.x * blockDim.x) {
     // pair -> (j, k)
     const double b = 2.0 * N - 1.0;
     long long j = (long long)floor(0.5 * (b - sqrt(fmax(b * b - 8.0 * (double)p, 0.0))));
@@ -265,6 +284,7 @@ __global__ void large_coef(LargeEval E) {
     while (j < N - 2 && (j + 1) * N - (j + 1) * (j + 2) / 2 <= p) ++j;
     while (j > 0 && j * N - j * (j + 1) / 2 > p) --j;
     const long long k = p - (j * N - j * (j + 1) / 2) + j + 1;
+    if (!(j >= E.m0 || (k >= E.m0 && k < E.m1))) continue;  // shard: rows before m0 only in owned columns
     const double w = E.X[p];
     const double c = (w == 0.0) ? 0.0 : __ddiv_rn(w, z);
     if (E.wout) E.wout[p] = c;
@@ -297,7 +317,7 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
   __shared__ double sPr[GK][GM], sPi[GK][GM];
   __shared__ double sFr[GK][RB], sFi[GK][RB];
   const int N = E.N, d = E.d, K = E.K;
-  const int mb = blockIdx.x, rb = blockIdx.y, ch = blockIdx.z;
+  const int mb = blockIdx.x + E.m0 / GM, rb = blockIdx.y, ch = blockIdx.z;
   const int k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
   const int tid = threadIdx.x;
   const int tm = tid & 15, tr = tid >> 4;
@@ -311,7 +331,7 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
     for (int e = tid; e < GK * GM; e += 256) {
       const int kk = e / GM, c = e - kk * GM;
       const int k = k0 + kk, m = mb * GM + c;
-      const bool v = k < k_hi && m < N;
+      const bool v = k < k_hi && m < E.m1;
       sPr[kk][c] = v ? E.PR[(long long)k * N + m] : 0.0;
       if (CPLX) sPi[kk][c] = v ? E.PI[(long long)k * N + m] : 0.0;
     }
@@ -360,7 +380,7 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int row = rb * RB + tr + 16 * r, m = mb * GM + tm + 16 * c;
-      if (row < d && m < N) {
+      if (row < d && m < E.m1) {
         double* out = E.part + (long long)ch * E.dim + (long long)m * E.L;
         if (CPLX) {
           out[2 * row] = ar[r][c];
@@ -375,8 +395,8 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
 // ---- K6b: t chunk partials, thread per (chunk, m), ascending k (c*u add)
 __global__ void large_tsum(LargeEval E) {
   const int ch = blockIdx.y;
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= E.N) return;
+  const int m = E.m0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= E.m1) return;
   const int k_lo = (ch * E.N) / E.K, k_hi = ((ch + 1) * E.N) / E.K;
   double t = 0.0;
 #pragma unroll 16
@@ -386,8 +406,8 @@ __global__ void large_tsum(LargeEval E) {
 
 // ---- K7: chunk partials added left to right; grad = ((acc - t phi)/alpha)*2
 __global__ void large_finalize(LargeEval E) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= E.dim) return;
+  const long long e = (long long)E.m0 * E.L + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)E.m1 * E.L) return;
   const int m = (int)(e / E.L), q = (int)(e - (long long)m * E.L);
   double a = E.part[e], t = E.tpart[m];
   for (int ch = 1; ch < E.K; ++ch) {

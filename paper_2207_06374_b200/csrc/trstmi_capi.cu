@@ -77,6 +77,7 @@ struct trstmi_ctx {
   int* counter = nullptr;
   trstmi_large::Engine* large = nullptr;  // large-frame path engine (lazy)
   int large_workers = 8;                  // concurrent large-path trials (streams)
+  int shard_world = 1;                    // single-frame row-block sharding (trstmi_set_shard)
   std::string err;
 };
 
@@ -203,6 +204,22 @@ int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   CUDA_TRY(ctx, cudaMemcpy(mismatches, db.p, 8, cudaMemcpyDeviceToHost));
   return TRSTMI_OK;
+}
+
+static trstmi_large::Engine* large_engine(trstmi_ctx* ctx, cudaStream_t st);
+
+int trstmi_nccl_unique_id(char* out128) {
+  std::string e;
+  return trstmi_large::nccl_unique_id(out128, &e);
+}
+
+int trstmi_set_shard(trstmi_ctx* ctx, int world, int rank, const char* nccl_id) {
+  if (!ctx || world < 1 || rank < 0 || rank >= world) return TRSTMI_ERR_INVALID_ARG;
+  cudaSetDevice(ctx->device);
+  trstmi_large::Engine* E = large_engine(ctx, ctx->stream);
+  const int rc = trstmi_large::engine_set_shard(E, world, rank, nccl_id, &ctx->err);
+  if (rc == TRSTMI_OK) ctx->shard_world = world;
+  return rc;
 }
 
 int trstmi_kchunks(int field, int64_t d, int64_t N) { return kchunks_for((int)d, (int)N, trstmi_lanes(field, d, N)); }
@@ -581,15 +598,21 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
     // host workers, one CUDA stream + engine each, pull trial ids from an
     // atomic counter; each drives its trial's trust-region loop.
     CUDA_TRY(ctx, cudaStreamSynchronize(st));
-    const int workers = (int)std::max<int64_t>(1, std::min<int64_t>(trials, ctx->large_workers));
+    const int workers =
+        ctx->shard_world > 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(trials, ctx->large_workers));
     std::atomic<int64_t> next{0};
     std::vector<int> rcs(workers, TRSTMI_OK);
     std::vector<std::string> errs(workers);
     auto work = [&](int wi) {
       cudaSetDevice(ctx->device);
       cudaStream_t ws = nullptr;
-      cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking);
-      trstmi_large::Engine* E = trstmi_large::engine_create(ctx->device, ws);
+      trstmi_large::Engine* E = nullptr;
+      if (ctx->shard_world > 1) {  // the sharded engine (NCCL communicator / virtual ranks) of the context
+        E = large_engine(ctx, st);
+      } else {
+        cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking);
+        E = trstmi_large::engine_create(ctx->device, ws);
+      }
       for (int64_t t = next.fetch_add(1); t < trials && rcs[wi] == TRSTMI_OK; t = next.fetch_add(1)) {
         std::memset(&to[t], 0, sizeof(trstmi_trial_out));
         rcs[wi] = trstmi_large::anneal_trial(E, sh, tr, sched, 0, cap, params_dev + t * sh.dim,
@@ -598,8 +621,10 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
                                              so.data() + t * A.n_stages, oo.empty() ? nullptr : oo.data() + t * cap,
                                              &errs[wi]);
       }
-      trstmi_large::engine_destroy(E);
-      cudaStreamDestroy(ws);
+      if (ws) {
+        trstmi_large::engine_destroy(E);
+        cudaStreamDestroy(ws);
+      }
     };
     if (workers == 1) {
       work(0);
