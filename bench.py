@@ -38,11 +38,28 @@ sys.path.insert(0, ROOT)
 from paper_2207_06374_b200 import abi  # noqa: E402
 
 CONFIGS = {
-    # name: field, d, N, trials, max_outer
-    "c1": (abi.REAL, 4, 10, 64, 200),
-    "c2": (abi.COMPLEX, 2, 100, 4096, 500),
-    "c3": (abi.COMPLEX, 6, 36, 1024, 1000),
+    # name: field, d, N, trials per GPU, max_outer, workload
+    #   "anneal": the reference's full anneal (every delta stage)
+    #   "stage0": the anneal's first stage (delta = 0.1) with that max_outer —
+    #             the fixed-work mode SURVEY.md §8d prescribes for configs 4-5,
+    #             whose full anneals (CG up to 2*dim per iteration) cannot be timed
+    "c1": (abi.REAL, 4, 10, 64, 200, "anneal"),
+    "c2": (abi.COMPLEX, 2, 100, 4096, 500, "anneal"),
+    "c3": (abi.COMPLEX, 6, 36, 1024, 1000, "anneal"),
+    "c4": (abi.REAL, 64, 1024, 256, 300, "stage0"),
+    "c5": (abi.COMPLEX, 128, 4096, 64, 100, "stage0"),
+    # config 5's single frame, Gram row-blocks sharded over the ranks (NCCL)
+    "c5frame": (abi.COMPLEX, 128, 4096, 1, 20, "stage0"),
 }
+
+
+def make_cfg(field, d, N, max_outer, workload):
+    cfg = abi.default_cfg(field, d, N, max_outer)
+    if workload == "stage0":
+        from paper_2207_06374_b200 import api
+        cfg.n_stages = 1
+        cfg.schedule[0] = api.default_schedule(N)[0]
+    return cfg
 METRIC = "TR iterations/sec & Gram entries/sec (fp64, batched trials); % of roofline"
 
 
@@ -97,12 +114,12 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(field, d, N, max_outer, trials, threads, first=0):
-    """Oracle (port of the reference algorithm) over `trials` full anneals on
+def cpu_sample(field, d, N, max_outer, trials, threads, first=0, workload="anneal"):
+    """Oracle (port of the reference algorithm) over `trials` anneals on
     `threads` host threads; returns (seconds, outer iterations, evals)."""
     from tests import oracle_ffi as orc
     L = orc.lib()
-    cfg = abi.default_cfg(field, d, N, max_outer)
+    cfg = make_cfg(field, d, N, max_outer, workload)
     S = abi.lanes_for(field, d, N)
     params, st = orc.random_frames(field, d, N, 0, first, trials)
     outer = ctypes.c_int64()
@@ -116,15 +133,17 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU implementation of the reference algorithm."""
     if rank != 0:
         return
-    field, d, N, trials, max_outer = CONFIGS[args.config]
+    field, d, N, trials, max_outer, workload = CONFIGS[args.config]
+    if workload == "stage0":
+        max_outer = min(max_outer, args.cpu_outer)
     threads = os.cpu_count() or 1
-    sample = args.cpu_trials or threads
+    sample = args.cpu_trials or (threads if N <= 200 else min(threads, 4))
     n = N * (N - 1) // 2
     for _ in range(args.warmup):
-        cpu_sample(field, d, N, max_outer, min(sample, threads), threads)
+        cpu_sample(field, d, N, max_outer, min(sample, threads), threads, workload=workload)
     secs, outs, evs = [], [], []
     for _ in range(args.steps):
-        s, o, e = cpu_sample(field, d, N, max_outer, sample, threads)
+        s, o, e = cpu_sample(field, d, N, max_outer, sample, threads, workload=workload)
         secs.append(s)
         outs.append(o)
         evs.append(e)
@@ -157,6 +176,7 @@ def main():
     ap.add_argument("--trials", type=int, default=0, help="override trials per rank (testing only)")
     ap.add_argument("--cpu-trials", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-outer", type=int, default=3, help="stage0 configs: outer iterations per CPU sample trial")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -174,7 +194,7 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    field, d, N, trials, max_outer = CONFIGS[args.config]
+    field, d, N, trials, max_outer, workload = CONFIGS[args.config]
     if args.trials:
         trials = args.trials
     dim = abi.dim_of(field, d, N)
@@ -184,9 +204,15 @@ def main():
     lib.trstmi_launch_count.restype = ctypes.c_longlong
     lib.trstmi_measure_dfma_peak.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
     ctx = api.Context(local_rank)
-    cfg = abi.default_cfg(field, d, N, max_outer)
-    ns = api.default_schedule_len(N)
+    cfg = make_cfg(field, d, N, max_outer, workload)
+    ns = cfg.n_stages or api.default_schedule_len(N)
     first = rank * trials
+    sharded = args.config == "c5frame"
+    if sharded and world > 1:  # one frame, Gram row-blocks over the ranks
+        obj = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.set_shard(world, rank, obj[0])
+        first = 0
 
     # inputs: start frames + generator states (host, pinned for e2e)
     starts, rng0 = api.random_frames(field, d, N, 0, first, trials)
@@ -218,8 +244,8 @@ def main():
 
     def reduce_best():
         """min over trials then over ranks, lowest trial id on ties (solver.hpp:256-263)."""
-        ctypes.memmove(h_tout, d_tout.data_ptr() if False else d_tout.cpu().numpy().ctypes.data,
-                       ctypes.sizeof(h_tout))
+        host = d_tout.cpu().numpy()  # keep the host copy alive across the memmove
+        ctypes.memmove(h_tout, host.ctypes.data, ctypes.sizeof(h_tout))
         best, bi = None, -1
         for t in range(trials):
             r = h_tout[t]
@@ -260,6 +286,8 @@ def main():
         w = torch.tensor([tot_outer, tot_evals], dtype=torch.float64, device="cuda")
         dist.all_reduce(w)
         tot_outer_all, tot_evals_all = int(w[0].item()), int(w[1].item())
+        if sharded:  # the ranks processed one frame together
+            tot_outer_all, tot_evals_all = tot_outer, tot_evals
         cand = torch.tensor([best_mu if best_mu is not None else float("inf"), float(first + best_trial)],
                             dtype=torch.float64, device="cuda")
         allc = [torch.empty_like(cand) for _ in range(world)]
@@ -321,30 +349,34 @@ def main():
     cpu = None
     if not args.no_cpu and world == 1:
         threads = os.cpu_count() or 1
-        sample = args.cpu_trials or threads
-        s, o, e = cpu_sample(field, d, N, max_outer, sample, threads)
+        sample = args.cpu_trials or (threads if N <= 200 else min(threads, 4))
+        cpu_outer = max_outer if workload == "anneal" else min(max_outer, args.cpu_outer)
+        s, o, e = cpu_sample(field, d, N, cpu_outer, sample, threads, workload=workload)
         cpu = {"value": o / s, "unit": "TR iterations/s", "cores": threads, "kind": "port",
-               "sample": "%d full anneals of this workload (trials 0..%d) on %d host threads, %.1f s; "
-                         "oracle/ CAS restatement (reference not buildable: no Eigen)" % (sample, sample - 1,
-                                                                                          threads, s),
+               "sample": "%d %s of this workload (trials 0..%d) on %d host threads, %.1f s; "
+                         "oracle/ CAS restatement (reference not buildable: no Eigen)"
+                         % (sample, "full anneals" if workload == "anneal" else
+                            "stage-0 runs capped at %d outer iterations" % cpu_outer, sample - 1, threads, s),
                "gram_entries_per_s": e * n / s}
 
     value = tot_outer_all / t_all
     line = {
         "metric": METRIC, "value": value, "unit": "TR iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "gram_entries_per_s": tot_evals_all * n / t_all, "evals_per_s": tot_evals_all / t_all,
-        "config": {"workload": "%s: %s lines d=%d N=%d, %d trials/GPU x anneal(max_outer=%d, eps 1e-7, %d stages)"
-                   % (args.config, "complex" if field == abi.COMPLEX else "real", d, N, trials, max_outer, ns),
+        "config": {"workload": "%s: %s lines d=%d N=%d, %d trials/GPU x %s(max_outer=%d, eps 1e-7, %d stage%s)"
+                   % (args.config, "complex" if field == abi.COMPLEX else "real", d, N, trials,
+                      "anneal" if workload == "anneal" else "anneal stage 0", max_outer, ns, "s" if ns > 1 else ""),
                    "trials_per_gpu": trials, "max_outer": max_outer, "seed": 0,
                    "l2": "flushed (256 MB write) before every timed step; inputs 13 MB",
-                   "parallelism": "trials sharded over %d GPU(s), NCCL allgather(best mu)+broadcast(frame)" % world},
+                   "parallelism": ("one frame, Gram row-blocks sharded over %d GPU(s) (NCCL)" % world) if sharded else
+                                  ("trials sharded over %d GPU(s), NCCL allgather(best mu)+broadcast(frame)" % world)},
         "best_mu": best_mu, "best_trial": gbest,
         "welch_bound": api.welch_bound(d, N),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": achieved / peak.value, "traffic": traffic, "traffic_unit": "bytes/launch",
-                     "note": "achieved = evals x 16dN^2 (dense contraction count, SURVEY 8d) / anneal-kernel time; "
+                     "note": "achieved = evals x (16|4)dN^2 (dense contraction count, SURVEY 8d) / step device time; "
                              "peak = DFMA-loop throughput measured live on this GPU (MEASURED_PEAKS.json has no FP64)"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "cpu_baseline": cpu,
     }

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <atomic>
 #include <map>
 
 #include <nccl.h>
@@ -15,6 +16,8 @@
 using namespace trstmi_dev;
 
 namespace trstmi_large {
+
+std::atomic<long long> g_large_launches{0};  // kernels launched by the large-frame engine
 
 namespace {
 
@@ -51,6 +54,8 @@ struct Engine {
   int* flag = nullptr;
   double* h_scal = nullptr;  // pinned: [0..3] dots / scalars, [4] zero col
 };
+
+long long launches() { return g_large_launches.load(); }
 
 Shape make_shape(int field, int d, int N) {
   Shape s;
@@ -218,6 +223,7 @@ int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double 
   else large_grad_gemm<false><<<gg, 256, 0, st>>>(L);
   large_tsum<<<dim3((sh.N + 127) / 128, sh.K), 128, 0, st>>>(L);
   large_finalize<<<(sh.dim + 255) / 256, 256, 0, st>>>(L);
+  g_large_launches += 9;
   LCHK(cudaGetLastError());
   LCHK(cudaMemcpyAsync(E->h_scal, w.scal, 3 * 8, cudaMemcpyDeviceToHost, st));
   LCHK(cudaMemcpyAsync(E->h_scal + 4, w.zero_col, 4, cudaMemcpyDeviceToHost, st));
@@ -351,6 +357,7 @@ static int eval_sharded(Engine* E, const Shape& sh, const double* x, const doubl
     }
   }
   LCHK(cudaGetLastError());
+  g_large_launches += (long long)ranks.size() * 9;
   if (!E->virtual_ranks) {  // gradient column slices to every rank
     NCHK(ncclGroupStart());
     for (int r = 0; r < G; ++r) {
@@ -410,6 +417,7 @@ static int dots(Engine* E, long long n, int nd, const double* a0, const double* 
   large_dots<<<LS_CTAS, LS_THREADS, 0, E->st>>>(a0, b0, a1 ? a1 : a0, b1 ? b1 : b0, a2 ? a2 : a0, b2 ? b2 : b0, nd,
                                                 n, E->dots_cta);
   large_dots_reduce<<<1, LS_CTAS, 0, E->st>>>(E->dots_cta, nd, E->dots_out);
+  g_large_launches += 2;
   LCHK(cudaGetLastError());
   LCHK(cudaMemcpyAsync(E->h_scal, E->dots_out, nd * 8, cudaMemcpyDeviceToHost, E->st));
   LCHK(cudaStreamSynchronize(E->st));

@@ -17,6 +17,8 @@ namespace trstmi_large {
 
 constexpr int kLanes = 32768;
 
+long long launches();  // kernels launched by the large-frame engine so far
+
 struct Shape {
   int cplx, d, N, L, dim, K;
   long long n;

@@ -150,7 +150,7 @@ extern "C" {
 
 int trstmi_version(void) { return 1; }
 
-long long trstmi_launch_count(void) { return g_launches; }
+long long trstmi_launch_count(void) { return g_launches + trstmi_large::launches(); }
 
 // Measured FP64 FMA peak of the device (TFLOP/s, 2 flops per fma), timed with
 // CUDA events over `iters` x 128 fma per thread on a full-occupancy grid.
