@@ -135,9 +135,9 @@ def run_reference(args, rank, world):
         return
     field, d, N, trials, max_outer, workload = CONFIGS[args.config]
     if workload == "stage0":
-        max_outer = min(max_outer, args.cpu_outer)
+        max_outer = min(max_outer, args.cpu_outer or (1 if N > 2048 else 3))
     threads = os.cpu_count() or 1
-    sample = args.cpu_trials or (threads if N <= 200 else min(threads, 4))
+    sample = args.cpu_trials or threads
     n = N * (N - 1) // 2
     for _ in range(args.warmup):
         cpu_sample(field, d, N, max_outer, min(sample, threads), threads, workload=workload)
@@ -157,7 +157,7 @@ def run_reference(args, rank, world):
         "config": {"workload": "%s: %s d=%d N=%d, %d trials x anneal(max_outer=%d); CPU sample %d trials/step"
                    % (args.config, "complex" if field == abi.COMPLEX else "real", d, N, trials, max_outer, sample),
                    "trials": trials, "max_outer": max_outer, "seed": 0},
-        "cpu_baseline": {"value": v, "unit": "TR iterations/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "TR iterations/s", "cores": min(sample, threads), "kind": "port",
                          "sample": "%d full anneals (trials 0..%d of the seed-0 batch) per step on %d threads; "
                                    "oracle/ CAS restatement (reference not buildable: no Eigen)"
                                    % (sample, sample - 1, threads)},
@@ -176,7 +176,8 @@ def main():
     ap.add_argument("--trials", type=int, default=0, help="override trials per rank (testing only)")
     ap.add_argument("--cpu-trials", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-outer", type=int, default=3, help="stage0 configs: outer iterations per CPU sample trial")
+    ap.add_argument("--cpu-outer", type=int, default=0,
+                    help="stage0 configs: outer iterations per CPU sample trial (default 3; 1 when N > 2048)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -349,10 +350,10 @@ def main():
     cpu = None
     if not args.no_cpu and world == 1:
         threads = os.cpu_count() or 1
-        sample = args.cpu_trials or (threads if N <= 200 else min(threads, 4))
-        cpu_outer = max_outer if workload == "anneal" else min(max_outer, args.cpu_outer)
+        sample = args.cpu_trials or threads
+        cpu_outer = max_outer if workload == "anneal" else min(max_outer, args.cpu_outer or (1 if N > 2048 else 3))
         s, o, e = cpu_sample(field, d, N, cpu_outer, sample, threads, workload=workload)
-        cpu = {"value": o / s, "unit": "TR iterations/s", "cores": threads, "kind": "port",
+        cpu = {"value": o / s, "unit": "TR iterations/s", "cores": min(sample, threads), "kind": "port",
                "sample": "%d %s of this workload (trials 0..%d) on %d host threads, %.1f s; "
                          "oracle/ CAS restatement (reference not buildable: no Eigen)"
                          % (sample, "full anneals" if workload == "anneal" else

@@ -25,6 +25,10 @@ constexpr double kFdBaseStep = 0x1.965fea53d6e3dp-18;  // smoothing.hpp:16-17 (g
 constexpr double kUnderflowCut = -746.0;               // exp((x-s)/delta) == 0 below this * delta
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef TRSTMI_EXP
+#define TRSTMI_EXP cas_exp  // experiments may substitute a stub (scripts/phase_timers.sh)
+#endif
+
 #ifdef TRSTMI_PHASE_TIMERS
 __device__ unsigned long long g_phase_cycles[8];
 #define PHASE_MARK(i)                                                        \
@@ -487,7 +491,7 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
           if (div_needs_ieee(diff[u])) y[u] = __ddiv_rn(diff[u], delta);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) w[u] = (diff[u] >= cut) ? cas_exp(y[u]) : 0.0;
+      for (int u = 0; u < 4; ++u) w[u] = (diff[u] >= cut) ? TRSTMI_EXP(y[u]) : 0.0;
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u) w[u] = 0.0;

@@ -37,6 +37,6 @@ int main(int argc, char** argv) {
   for (int i = 0; i < 6; ++i) printf("  %-10s %8.0f\n", names[i], c[i] / (double)B);
 }
 CU
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false --expt-relaxed-constexpr -DDD=$2 -DSS=${5:-512} \
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false --expt-relaxed-constexpr -DDD=$2 -DSS=${5:-512} $EXTRA \
   -I paper_2207_06374_b200/csrc -I include -o /tmp/phase/pt /tmp/phase/pt.cu
 /tmp/phase/pt "$@"
