@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
         for (int j = tid; j < P.N; j += S) {
           double acc = 0.0;
           for (int q = 0; q < P.L; ++q) acc = fma(x[j * P.L + q], x[j * P.L + q], acc);
-          if (sqrt(acc) < kZeroColumnTol) zc = min(zc, j);
+          if (!(sqrt(acc) >= kZeroColumnTol)) zc = min(zc, j);  // NaN norms are rescued too (solver.hpp:144)
         }
         zc = block_min_int<S>(zc, sm.ired, rbuf);
         if (zc != INT_MAX) {

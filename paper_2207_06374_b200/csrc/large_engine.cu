@@ -580,7 +580,7 @@ int anneal_trial(Engine* E, const Shape& sh, const TrCfg& tr, const std::vector<
     LCHK(cudaStreamSynchronize(st));
     bool any_zero = false;
     for (int j = 0; j < sh.N && !any_zero; ++j)
-      any_zero = trstmi_host::column_norm(&host[(size_t)j * sh.L], sh.L) < trstmi_host::kZeroColumnTol;
+      any_zero = !(trstmi_host::column_norm(&host[(size_t)j * sh.L], sh.L) >= trstmi_host::kZeroColumnTol);
     if (any_zero) {
       const int bad = trstmi_host::rescue_zero_columns(sh.cplx, sh.d, sh.N, host.data(), rng_state ? &rng : nullptr);
       if (bad >= 0) {

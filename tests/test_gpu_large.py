@@ -94,3 +94,66 @@ def test_large_anneal_trajectory_bit_exact(ctx, field, d, N, trials, max_outer):
     g = ctx.solve_batch(cfg, starts, st)
     o = orc.solve_batch(cfg, S, starts, st, threads=2)
     _cmp_solve(g, o, trials, 3, 400)
+
+
+def test_large_zero_column_paths(ctx):
+    """ZeroColumnError semantics on the large path: eval -> (+inf, 0); the
+    HVP one-sided fallback (solver.hpp:118-137); stage-boundary rescue."""
+    from paper_2207_06374_b200 import api
+    field, d, N = C, 18, 40
+    S = api.lanes(field, d, N)
+    x = orc.random_test_frame(field, d, N, 9)
+    L = 2 * d
+    x0 = x.copy()
+    x0[3 * L:4 * L] = 0.0  # column 3 is zero
+    F, s, g, w, zc = ctx.eval_batch(field, d, N, x0[None], 1e-2)
+    assert zc[0] == 3 and np.isinf(F[0]) and not g.any()
+    # a column at the FD step scale forces the fallback
+    kfd = float.fromhex('0x1.965fea53d6e3dp-18')
+    xf = x.copy()
+    dirv = np.zeros_like(x)
+    dirv[0] = -1.0
+    xf[0:L] = 0.0
+    for _ in range(3):
+        xf[0] = kfd * (1.0 + np.linalg.norm(xf)) / np.linalg.norm(dirv)
+    hv, path, zcol = ctx.hvp_batch(field, d, N, xf[None], dirv[None], 1e-1)
+    ho, po, zo = orc.hvp(field, d, N, S, xf, dirv, 1e-1)
+    assert path[0] == po and po in (abi.HVP_FORWARD, abi.HVP_BACKWARD)
+    assert np.array_equal(bits(hv[0]), bits(ho))
+    # rescue at the stage boundary with the trial's generator; without it the trial fails
+    cfg = abi.default_cfg(field, d, N, 3)
+    cfg.n_stages = 2
+    sched = api.default_schedule(N)
+    cfg.schedule[0], cfg.schedule[1] = sched[0], sched[1]
+    rng = np.array([[8, 0, 0]], np.uint64)
+    g = ctx.solve_batch(cfg, x0[None], rng)
+    o = orc.solve_batch(cfg, S, x0[None], rng, threads=1)
+    assert g["trials"][0].status == o["trials"][0].status == abi.TRIAL_OK
+    assert np.array_equal(bits(g["frames"]), bits(o["frames"]))
+    assert np.array_equal(g["rng"], o["rng"])
+    g2 = ctx.solve_batch(cfg, x0[None], None)
+    assert g2["trials"][0].status == abi.TRIAL_ZERO_COLUMN and g2["trials"][0].zero_col == 3
+
+
+def test_large_magnitude_mode_bit_exact(ctx):
+    from paper_2207_06374_b200 import api
+    field, d, N = R, 20, 60
+    S = api.lanes(field, d, N)
+    x = orc.random_test_frame(field, d, N, 4)
+    F, s, g, w, zc = ctx.eval_batch(field, d, N, x[None], 1e-1, False, True)
+    Fo, so, go, wo, zo = orc.eval_objective(field, d, N, S, x, 1e-1, squared=False, want_weights=True)
+    assert bits(F[0]) == bits(Fo) and np.array_equal(bits(g[0]), bits(go)) and np.array_equal(bits(w[0]), bits(wo))
+
+
+def test_large_solve_known_optimum_structure(ctx):
+    """solve() through the large path at a shape with a known bound: mu never
+    below Welch (test_solver.cpp:151-163)."""
+    from paper_2207_06374_b200 import api
+    field, d, N = C, 17, 30
+    cfg = abi.default_cfg(field, d, N, 20)
+    cfg.eps_target = 1e-3
+    starts, st = api.random_frames(field, d, N, 5, 0, 2)
+    g = ctx.solve_batch(cfg, starts, st)
+    for t in range(2):
+        assert g["trials"][t].status == abi.TRIAL_OK
+        assert g["trials"][t].coherence >= api.welch_bound(d, N) - 1e-9

@@ -222,3 +222,34 @@ def test_markstein_division_matches_ieee(ctx):
     bad = ctypes.c_uint64()
     assert lib.trstmi_selftest_division(ctx.h, 1 << 31, 20250809, ctypes.byref(bad)) == 0
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("field,d,N", [(C, 1, 2), (R, 1, 2), (C, 5, 2), (R, 16, 3), (C, 16, 17)])
+def test_edge_shapes_bit_exact(ctx, field, d, N):
+    """Smallest pair counts (N = 2: one pair), d = 1, and the runtime-d kernel family (d = 16)."""
+    from paper_2207_06374_b200 import api
+    S = api.lanes(field, d, N)
+    pts = np.stack([orc.random_test_frame(field, d, N, s) for s in (1, 2)])
+    for delta in (1e-1, 1e-7):
+        F, s, g, w, zc = ctx.eval_batch(field, d, N, pts, delta, True, True)
+        for b in range(2):
+            Fo, so, go, wo, zo = orc.eval_objective(field, d, N, S, pts[b], delta, want_weights=True)
+            assert bits(F[b]) == bits(Fo) and np.array_equal(bits(g[b]), bits(go))
+    cfg = abi.default_cfg(field, d, N, 30)
+    cfg.record_cap = 300
+    starts, st = api.random_frames(field, d, N, 0, 0, 3)
+    _cmp_solve(ctx.solve_batch(cfg, starts, st), orc.solve_batch(cfg, S, starts, st, threads=3), 3,
+               api.default_schedule_len(N), 300)
+
+
+def test_nonfinite_start_fails_like_the_reference(ctx):
+    """A NaN entry makes the stage's x0 evaluation non-finite:
+    trust_region_minimize throws invalid_argument (trust_region.hpp:206-209)."""
+    from paper_2207_06374_b200 import api
+    cfg = abi.default_cfg(C, 2, 6, 10)
+    starts, st = api.random_frames(C, 2, 6, 0, 0, 2)
+    starts[1, 3] = np.nan
+    g = ctx.solve_batch(cfg, starts, st)
+    o = orc.solve_batch(cfg, api.lanes(C, 2, 6), starts, st, threads=2)
+    assert g["trials"][0].status == o["trials"][0].status == abi.TRIAL_OK
+    assert g["trials"][1].status == o["trials"][1].status
