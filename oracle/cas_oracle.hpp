@@ -90,11 +90,16 @@ constexpr double kFdBaseStep = 0x1.965fea53d6e3dp-18;  // smoothing.hpp:16-17, g
 constexpr double kUnderflowCut = -746.0;
 
 // ---------------------------------------------------------------- CAS math
-// CAS exp: Cody-Waite reduction with an fma split of ln2, degree-13 Taylor in
-// Horner/fma form, exponent scaling by exact powers of two (one rounding for
-// subnormal results).  Bit-identical to the device cas_exp in
-// paper_2207_06374_b200/csrc/cas_math.cuh.  <= 1 ulp from glibc exp in the
-// tests (tests/test_oracle_math.py).
+// CAS exp: k = round-to-nearest-even(x log2 e) by the fma magic-constant
+// trick (t = fma(x, log2e, 1.5*2^52), kd = t - 1.5*2^52, k = low word of t),
+// Cody-Waite reduction with an fma split of ln2, degree-13 Taylor in
+// Horner/fma form, scaling (p * 2^(k>>1)) * 2^(k-(k>>1)) (the first product
+// exact, one rounding, also for subnormal results).  cas_exp_core is the
+// formula on [-746.25, 709.78]; cas_exp adds NaN / overflow / underflow.
+// No rint/float<->int conversion and no compares in the core: those run at
+// 1/4 of the FP64 rate on B200 (scripts/micro/fp64_ops.cu).  Bit-identical to
+// the device cas_exp in paper_2207_06374_b200/csrc/cas_math.cuh; <= 1 ulp
+// from glibc exp in the tests (tests/test_oracle_cpu.py).
 inline double pow2i(int k) {  // 2^k for -1022 <= k <= 1023, exact
   std::uint64_t bits = static_cast<std::uint64_t>(k + 1023) << 52;
   double r;
@@ -102,10 +107,13 @@ inline double pow2i(int k) {  // 2^k for -1022 <= k <= 1023, exact
   return r;
 }
 
-inline double cas_exp(double x) {
-  const double xc = std::fmin(std::fmax(x, -745.25), 709.8);
-  const double kd = std::nearbyint(xc * 1.4426950408889634);
-  double r = std::fma(-kd, 6.93147180369123816490e-01, xc);
+inline double cas_exp_core(double x) {
+  const double t = std::fma(x, 1.4426950408889634, 0x1.8p52);
+  const double kd = t - 0x1.8p52;
+  std::uint64_t tb;
+  std::memcpy(&tb, &t, 8);
+  const int k = static_cast<int>(static_cast<std::uint32_t>(tb));  // low word = k (two's complement)
+  double r = std::fma(-kd, 6.93147180369123816490e-01, x);
   r = std::fma(-kd, 1.90821492927058770002e-10, r);
   double p = 1.6059043836821613e-10;            // 1/13!
   p = std::fma(p, r, 2.08767569878680989792e-09);  // 1/12!
@@ -121,12 +129,15 @@ inline double cas_exp(double x) {
   p = std::fma(p, r, 0.5);
   p = std::fma(p, r, 1.0);
   p = std::fma(p, r, 1.0);
-  const int k = static_cast<int>(kd);
   const int k1 = k >> 1;  // arithmetic shift: floor(k / 2)
-  double res = (p * pow2i(k1)) * pow2i(k - k1);  // exact, then one rounding
-  if (x > 709.782712893383973096) res = std::numeric_limits<double>::infinity();
-  if (x < -745.2) res = 0.0;
-  return (x == x) ? res : x;
+  return (p * pow2i(k1)) * pow2i(k - k1);  // exact, then one rounding
+}
+
+inline double cas_exp(double x) {
+  if (!(x == x)) return x;
+  if (x > 709.782712893383973096) return std::numeric_limits<double>::infinity();
+  if (x < -746.25) return 0.0;
+  return cas_exp_core(x);
 }
 
 // CAS log (used once per evaluation, for F = s + delta*log z with z >= 1):

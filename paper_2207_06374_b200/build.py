@@ -22,7 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
                  "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I", os.path.join(HERE, "..", "include")]
 
-INSTANCES = [(c, s) for c in (1, 0) for s in (32, 128, 256)]
+# (complex, S, stored-Gram layout): the set kernel_table.hpp declares
+INSTANCES = [(c, s, g) for c in (1, 0) for (s, g) in ((32, 1), (128, 1), (128, 0), (256, 1), (256, 0), (512, 1))]
 
 
 def _run(cmd):
@@ -58,10 +59,10 @@ def build(verbose=False, force=False, jobs=None):
     jobs = jobs or max(2, min(8, os.cpu_count() or 2))
     tasks = []
     objs = []
-    for cplx, s in INSTANCES:
-        o = os.path.join(BUILD, "inst_%s_%d.o" % ("c" if cplx else "r", s))
+    for cplx, s, g in INSTANCES:
+        o = os.path.join(BUILD, "inst_%s_%d_%s.o" % ("c" if cplx else "r", s, "g" if g else "r"))
         objs.append(o)
-        tasks.append(COMMON + ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-c",
+        tasks.append(COMMON + ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-DINST_GS=%d" % g, "-c",
                                os.path.join(CSRC, "instantiate.cu"), "-o", o])
     for src in ("trstmi_capi.cu", "large_engine.cu"):
         o = os.path.join(BUILD, src.replace(".cu", ".o"))

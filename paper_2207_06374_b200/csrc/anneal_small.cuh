@@ -14,7 +14,7 @@
 // evaluated redundantly (and identically) by every thread of the CTA from
 // CTA-reduced values, so all branches are block-uniform.
 #pragma once
-#include "small_path.cuh"
+#include "small_gs.cuh"
 
 namespace trstmi_dev {
 
@@ -53,12 +53,23 @@ template <bool CPLX>
 __device__ __forceinline__ void carve(const Prob& P, int S, double* base, Smem& sm, double** vecs, int nvec) {
   const int W = S / 32;
   double* p = base;
+  if (P.gs) {  // stored-Gram layout (small_gs.cuh), 16-byte aligned arrays first; pair_smem_doubles() counts it
+    sm.GRI = p;
+    p += ((long long)P.np * (CPLX ? 2 : 1) + 1) & ~1LL;
+    sm.phiC = p;
+    p += ((long long)gs_col_stride(P.L) * P.N + 1) & ~1LL;
+    sm.fk = reinterpret_cast<int*>(p);
+    p += (P.N + 1) / 2;
+  } else {
+    sm.GRI = sm.phiC = nullptr;
+    sm.fk = nullptr;
+  }
   sm.phiS = p;
   p += P.L * P.N;
   sm.alpha = p;
   p += P.N;
   sm.U = p;
-  p += P.n;
+  p += P.gs ? P.np : P.n;
   sm.part = p;
   p += (long long)P.K * P.N * (P.L + 1);
   sm.mask = reinterpret_cast<unsigned*>(p);
@@ -89,7 +100,7 @@ __device__ __forceinline__ int all_finite(const double* v, int n, const Smem& sm
   return block_min_int<S>(ok, sm.ired, rbuf);
 }
 
-template <bool CPLX, int DMAX, bool EXACT, int S>
+template <bool CPLX, int DMAX, bool EXACT, int S, bool GS>
 __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kernel(const AnnealArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   const Prob P = A.P;
@@ -98,7 +109,7 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
   Smem sm;
   double* v[9];
   carve<CPLX>(P, S, smem_raw, sm, v, 9);
-  build_pair_table<S>(P, sm.jk);
+  build_tables<S, CPLX, GS>(P, sm);
   double* x = v[0];   // current iterate
   double* g = v[1];   // current gradient
   double* zs = v[2];  // Steihaug step z
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
       // ---- x0 evaluation (trust_region.hpp:206-209)
       double Fcur;
       ++evals;
-      const int zc0 = eval_cta<CPLX, DMAX, EXACT, S>(P, x, nullptr, 0.0, delta, sm, rbuf, g, &sm.scal[0], nullptr, nullptr);
+      const int zc0 = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, nullptr, 0.0, delta, sm, rbuf, g, &sm.scal[0], nullptr, nullptr);
       Fcur = sm.scal[0];
       (void)zc0;
       {
@@ -209,9 +220,9 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
               const double h = kFdBaseStep * (1.0 + xnorm) / fmax(dn, 1e-300);
               __syncthreads();
               evals += 2;
-              const int zp = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, h, delta, sm, rbuf, bd, nullptr, nullptr, nullptr);
+              const int zp = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, dv, h, delta, sm, rbuf, bd, nullptr, nullptr, nullptr);
               if (zp < 0) {
-                const int zm = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
+                const int zm = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
                 if (zm < 0) {
                   const double h2 = 2.0 * h;
                   for (int i = tid; i < dim; i += S) bd[i] = (bd[i] - gt[i]) / h2;
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
                 }
               } else {  // x+hd hit a zero column: g0, retry forward (fails again), backward
                 evals += 2;
-                const int zm = eval_cta<CPLX, DMAX, EXACT, S>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
+                const int zm = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
                 if (zm >= 0) {
                   status = TRSTMI_TRIAL_ZERO_COLUMN;
                   zero_col = zm;
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
           __syncthreads();
           ++evals;
           double Ft;
-          eval_cta<CPLX, DMAX, EXACT, S>(P, xt, nullptr, 0.0, delta, sm, rbuf, gt, &sm.scal[0], nullptr, nullptr);
+          eval_any<CPLX, DMAX, EXACT, S, GS>(P, xt, nullptr, 0.0, delta, sm, rbuf, gt, &sm.scal[0], nullptr, nullptr);
           Ft = sm.scal[0];
           const int gfin = all_finite<S>(gt, dim, sm, rbuf);
           const bool finite = isfinite(Ft) && gfin;
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
       // ---- stage record: coherence(normalize_columns(param)) (solver.hpp:197)
       double smu;
       long long sarg;
-      const int zc = coherence_cta<CPLX, DMAX, EXACT, S>(P, x, true, sm, rbuf, &smu, &sarg);
+      const int zc = coherence_cta<CPLX, DMAX, EXACT, S, GS>(P, x, true, sm, rbuf, &smu, &sarg);
       if (zc >= 0) {
         status = TRSTMI_TRIAL_ZERO_COLUMN;
         zero_col = zc;

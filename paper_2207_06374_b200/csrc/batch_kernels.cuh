@@ -26,22 +26,22 @@ struct BatchArgs {
   long long* argmax;     // B (coherence)
 };
 
-template <bool CPLX, int DMAX, bool EXACT, int S>
+template <bool CPLX, int DMAX, bool EXACT, int S, bool GS>
 __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) eval_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[3];
   carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
-  build_pair_table<S>(A.P, sm.jk);
+  build_tables<S, CPLX, GS>(A.P, sm);
   int rbuf = 0;
   for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
     const double* x = A.pts + b * A.P.dim;
     double F, s;
     double* wo = A.weights ? A.weights + b * A.P.n : nullptr;
     const int zc = A.squared
-                       ? eval_cta<CPLX, DMAX, EXACT, S, true>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf,
+                       ? eval_any<CPLX, DMAX, EXACT, S, GS, true>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf,
                                                               A.out + b * A.P.dim, &sm.scal[0], &sm.scal[1], wo)
-                       : eval_cta<CPLX, DMAX, EXACT, S, false>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf,
+                       : eval_any<CPLX, DMAX, EXACT, S, GS, false>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf,
                                                                A.out + b * A.P.dim, &sm.scal[0], &sm.scal[1], wo);
     F = sm.scal[0];
     s = sm.scal[1];
@@ -56,13 +56,13 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) eval_batch_kernel
 
 // make_hvp_factory(obj)(x)(dir) (solver.hpp:118-137) around
 // fd_hessian_vector_product (smoothing.hpp:167-181).
-template <bool CPLX, int DMAX, bool EXACT, int S>
+template <bool CPLX, int DMAX, bool EXACT, int S, bool GS>
 __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) hvp_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[3];
   carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
-  build_pair_table<S>(A.P, sm.jk);
+  build_tables<S, CPLX, GS>(A.P, sm);
   double* gp = v[0];
   double* gm = v[1];
   double* g0 = v[2];
@@ -82,21 +82,21 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) hvp_batch_kernel(
       path = TRSTMI_HVP_ZERO_DIR;
     } else {
       const double h = kFdBaseStep * (1.0 + sqrt(nn[1])) / fmax(dn, 1e-300);
-      const int zp = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, h, delta, sm, rbuf, gp, nullptr, nullptr, nullptr);
+      const int zp = eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, dir, h, delta, sm, rbuf, gp, nullptr, nullptr, nullptr);
       if (zp < 0) {
-        const int zm = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
+        const int zm = eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
         if (zm < 0) {
           const double h2 = 2.0 * h;
           for (int i = threadIdx.x; i < dim; i += S) hv[i] = (gp[i] - gm[i]) / h2;
           path = TRSTMI_HVP_CENTRAL;
         } else {
-          eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, delta, sm, rbuf, g0, nullptr, nullptr, nullptr);
+          eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, nullptr, 0.0, delta, sm, rbuf, g0, nullptr, nullptr, nullptr);
           for (int i = threadIdx.x; i < dim; i += S) hv[i] = (gp[i] - g0[i]) / h;
           path = TRSTMI_HVP_FORWARD;
         }
       } else {
-        eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, nullptr, 0.0, delta, sm, rbuf, g0, nullptr, nullptr, nullptr);
-        const int zm = eval_cta<CPLX, DMAX, EXACT, S>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
+        eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, nullptr, 0.0, delta, sm, rbuf, g0, nullptr, nullptr, nullptr);
+        const int zm = eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
         if (zm < 0) {
           for (int i = threadIdx.x; i < dim; i += S) hv[i] = (g0[i] - gm[i]) / h;
           path = TRSTMI_HVP_BACKWARD;
@@ -115,18 +115,18 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) hvp_batch_kernel(
   }
 }
 
-template <bool CPLX, int DMAX, bool EXACT, int S>
+template <bool CPLX, int DMAX, bool EXACT, int S, bool GS>
 __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) coherence_batch_kernel(const BatchArgs A) {
   extern __shared__ __align__(16) double smem_raw[];
   Smem sm;
   double* v[1];
   carve<CPLX>(A.P, S, smem_raw, sm, v, 0);
-  build_pair_table<S>(A.P, sm.jk);
+  build_tables<S, CPLX, GS>(A.P, sm);
   int rbuf = 0;
   for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
     double mu = 0.0;
     long long arg = -1;
-    const int zc = coherence_cta<CPLX, DMAX, EXACT, S>(A.P, A.pts + b * A.P.dim, A.normalize != 0, sm, rbuf, &mu, &arg);
+    const int zc = coherence_cta<CPLX, DMAX, EXACT, S, GS>(A.P, A.pts + b * A.P.dim, A.normalize != 0, sm, rbuf, &mu, &arg);
     if (threadIdx.x == 0) {
       A.mu[b] = zc >= 0 ? 0.0 : mu;
       A.argmax[b] = zc >= 0 ? -1 : arg;

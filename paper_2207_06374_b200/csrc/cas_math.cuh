@@ -17,35 +17,41 @@ __device__ __forceinline__ double pow2i(int k) {  // 2^k, -1022 <= k <= 1023
   return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
 }
 
-// Branch-free so that several independent exps interleave in one thread.
-// The final scaling p * 2^k is done as (p * 2^(k>>1)) * 2^(k - (k>>1)): the
-// first product is exact, the second rounds once, so every result (normal,
-// subnormal or overflowing) is RN(p * 2^k).
-__device__ __forceinline__ double cas_exp(double x) {
-  const double xc = fmin(fmax(x, -745.25), 709.8);
-  const double kd = rint(__dmul_rn(xc, 1.4426950408889634));
-  double r = fma(-kd, 6.93147180369123816490e-01, xc);
-  r = fma(-kd, 1.90821492927058770002e-10, r);
-  double p = 1.6059043836821613e-10;
-  p = fma(p, r, 2.08767569878680989792e-09);
-  p = fma(p, r, 2.50521083854417187751e-08);
-  p = fma(p, r, 2.75573192239858906526e-07);
-  p = fma(p, r, 2.75573192239858906526e-06);
-  p = fma(p, r, 2.48015873015873015873e-05);
-  p = fma(p, r, 1.98412698412698412698e-04);
-  p = fma(p, r, 1.38888888888888888889e-03);
-  p = fma(p, r, 8.33333333333333333333e-03);
-  p = fma(p, r, 4.16666666666666666667e-02);
-  p = fma(p, r, 1.66666666666666666667e-01);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  const int k = static_cast<int>(kd);
+// k = RNE(x log2 e) by the fma magic-constant trick (no FRND / F2I: both run
+// at 1/4 of the DFMA rate on B200, scripts/micro/fp64_ops.cu); the scaling
+// (p * 2^(k>>1)) * 2^(k-(k>>1)) is exact in the first product and rounds once,
+// so every result (normal, subnormal or overflowing) is RN(p * 2^k).
+// cas_exp_core is the formula on [-746.25, 709.78] — no compares, so several
+// independent exps interleave; cas_exp adds the NaN / overflow / underflow
+// cases.  Operation-for-operation the oracle's cas_exp_core / cas_exp.
+// Polynomial / reduction constants in the constant bank: the DFMAs take them
+// as c[][] operands instead of two UMOVs per constant inside a large kernel.
+static __constant__ double kCasExpC[16] = {
+    1.6059043836821613e-10,  2.08767569878680989792e-09, 2.50521083854417187751e-08,
+    2.75573192239858906526e-07, 2.75573192239858906526e-06, 2.48015873015873015873e-05,
+    1.98412698412698412698e-04, 1.38888888888888888889e-03, 8.33333333333333333333e-03,
+    4.16666666666666666667e-02, 1.66666666666666666667e-01, 0.5, 1.0, 1.0,
+    6.93147180369123816490e-01, 1.90821492927058770002e-10};
+
+__device__ __forceinline__ double cas_exp_core(double x) {
+  const double t = fma(x, 1.4426950408889634, 0x1.8p52);
+  const double kd = __dsub_rn(t, 0x1.8p52);
+  const int k = __double2loint(t);  // low word of t = k (two's complement)
+  double r = fma(-kd, kCasExpC[14], x);
+  r = fma(-kd, kCasExpC[15], r);
+  double p = kCasExpC[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) p = fma(p, r, kCasExpC[i]);
   const int k1 = k >> 1;
-  double res = __dmul_rn(__dmul_rn(p, pow2i(k1)), pow2i(k - k1));
-  res = (x > 709.782712893383973096) ? __longlong_as_double(0x7ff0000000000000LL) : res;
-  res = (x < -745.2) ? 0.0 : res;
-  return (x == x) ? res : x;
+  return __dmul_rn(__dmul_rn(p, pow2i(k1)), pow2i(k - k1));
+}
+
+__device__ __forceinline__ double cas_exp(double x) {
+  const double res = cas_exp_core(fmin(fmax(x, -746.25), 709.79));  // identity on the core domain
+  if (!(x == x)) return x;
+  if (x > 709.782712893383973096) return __longlong_as_double(0x7ff0000000000000LL);
+  if (x < -746.25) return 0.0;
+  return res;
 }
 
 __device__ __forceinline__ double cas_log(double x) {

@@ -146,6 +146,9 @@ static int alloc_work(Work& w, const Shape& sh, std::string* err) {
   LCHK(cudaMalloc(&w.zero_col, 4));
   double** vecs[] = {&w.x, &w.g, &w.zs, &w.r, &w.dv, &w.bd, &w.xt, &w.gt, &w.xb, &w.zn, &w.gp, &w.gm};
   for (double** v : vecs) LCHK(cudaMalloc(v, (size_t)sh.dim * 8));
+  // the memsets above ran on the legacy stream, which the engine's
+  // non-blocking streams do not wait for
+  LCHK(cudaDeviceSynchronize());
   w.sh = sh;
   w.valid = true;
   return TRSTMI_OK;

@@ -28,6 +28,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef TRSTMI_EXP
 #define TRSTMI_EXP cas_exp  // experiments may substitute a stub (scripts/phase_timers.sh)
 #endif
+#ifndef TRSTMI_EXP_CORE
+#define TRSTMI_EXP_CORE cas_exp_core
+#endif
 
 #ifdef TRSTMI_PHASE_TIMERS
 __device__ unsigned long long g_phase_cycles[8];
@@ -55,7 +58,43 @@ struct BoolTag {
 struct Prob {
   int d, N, L, dim, n;  // L = doubles per column (2d complex, d real); n = pairs
   int K;                // CAS gradient k-chunks (trstmi_kchunks)
+  int gs;               // 1: stored-Gram layout (small_gs.cuh), 0: Gram recomputed in the gradient
+  int pad;              // gs: pair rows padded so both gradient orientations are bank-conflict free
+  int np;               // gs: physical pair slots (padded rows + one zero slot)
 };
+
+// Stored-Gram layout (small_gs.cuh): pair (a, b), a < b, lives in slot
+// rsp[a] + b - a - 1.  Every row is preceded by at least one zero slot, so
+// slot rsp[m] - 1 (what the k == m term of the gradient reads) is 0.  With
+// padding, f(a) = rsp[a] - a - 1 == a (mod 16), so the slot of (k, m) is
+// == k + m (mod 16) in both orientations: a warp reading pair (k, m) for 16
+// consecutive m hits 16 distinct 8-byte banks whether k < m (consecutive
+// slots of row k) or k > m (one slot in each of 16 rows).
+__host__ __device__ inline int gs_row_step(int N, int a, int pad) {
+  const int len = N - a - 1;
+  return pad ? len + (((1 - len) & 15) + 1) : len + 1;  // gap >= 1; step == 2 (mod 16) when padded
+}
+__host__ __device__ inline int gs_phys_slots(int N, int pad) {  // = rsp[N-1]
+  int r = 1;
+  for (int a = 0; a + 1 < N; ++a) r += gs_row_step(N, a, pad);
+  return r;
+}
+// column stride of the column-major phi copy: conflict-free 16-byte loads
+// for consecutive columns (and 8-byte loads when L is odd)
+__host__ __device__ inline int gs_col_stride(int L) { return (L % 4 == 0) ? L + 2 : L; }
+__host__ __device__ inline Prob make_small_prob(bool cplx, int d, int N, int K, int gs, int pad) {
+  Prob P;
+  P.d = d;
+  P.N = N;
+  P.L = (cplx ? 2 : 1) * d;
+  P.dim = P.L * N;
+  P.n = N * (N - 1) / 2;
+  P.K = K;
+  P.gs = gs;
+  P.pad = gs ? pad : 0;
+  P.np = gs ? gs_phys_slots(N, pad) : 0;
+  return P;
+}
 
 // CAS gradient chunk count K for a CTA of S threads: one
 // thread per (chunk, column), K = clamp(S / N, 1, 8).
@@ -283,7 +322,7 @@ __device__ __forceinline__ void for_pairs4(int N, int n, F&& f) {
 // Table-driven walk (the (j,k) of every pair is precomputed once per kernel
 // in Smem::jk as j | k << 16): warp-contiguous ranges, lanes step by 32,
 // four pairs per step.  f(p[4], j[4], k[4], valid[4]).
-template <int S, bool NEED_JK, class F>
+template <int S, bool NEED_JK, bool GS = false, class F>
 __device__ __forceinline__ void pairs4(int n, const unsigned* __restrict__ jk, F&& f) {
   constexpr int W = S / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -299,8 +338,13 @@ __device__ __forceinline__ void pairs4(int n, const unsigned* __restrict__ jk, F
       p[u] = v[u] ? p0 + 32 * u : p0;
       if constexpr (NEED_JK) {
         const unsigned t = jk[p[u]];
-        j[u] = (int)(t & 0xffffu);
-        k[u] = (int)(t >> 16);
+        if constexpr (GS) {  // stored-Gram table: phys | j << 16 | k << 24
+          j[u] = (int)((t >> 16) & 0xffu);
+          k[u] = (int)(t >> 24);
+        } else {
+          j[u] = (int)(t & 0xffffu);
+          k[u] = (int)(t >> 16);
+        }
       } else {
         j[u] = k[u] = 0;
       }
@@ -364,7 +408,10 @@ __device__ __forceinline__ bool div_needs_ieee(double a) { return a != 0.0 && fa
 struct Smem {
   double* phiS;      // L*N
   double* alpha;     // N
-  double* U;         // n
+  double* U;         // n (gs: np)
+  double* GRI;       // gs: np x C, (Re G, Im G) -> (c Re G, c Im G) per pair slot
+  double* phiC;      // gs: N x LP column-major copy of phi (LP = gs_col_stride(L))
+  int* fk;           // gs: N, f(a) = rsp[a] - a - 1 (slot of (k, m) = k < m ? f(k) + m : f(m) + k)
   double* part;      // K*N*(L+1)
   unsigned* mask;    // N*NW
   unsigned* jk;      // n: pair p -> j | k << 16
@@ -375,9 +422,10 @@ struct Smem {
 
 __host__ __device__ inline int mask_words(int N) { return (N + 31) / 32; }
 __host__ __device__ inline long long pair_smem_doubles(const Prob& P, bool cplx) {
-  (void)cplx;
-  return (long long)P.n + (long long)P.K * P.N * (P.L + 1) + ((long long)P.N * mask_words(P.N) + 1) / 2 +
-         ((long long)P.n + 1) / 2;
+  const long long common = (long long)P.K * P.N * (P.L + 1) + ((long long)P.N * mask_words(P.N) + 1) / 2 +
+                           ((long long)P.n + 1) / 2;
+  if (!P.gs) return (long long)P.n + common;
+  return (long long)P.np * (cplx ? 3 : 2) + (long long)gs_col_stride(P.L) * P.N + (P.N + 1) / 2 + 2 + common;
 }
 
 // Fills Smem::jk (once per kernel; ends with a barrier).
@@ -476,7 +524,7 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
     double diff[4], w[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) diff[u] = __dsub_rn(sm.U[p[u]], s);
-    const bool any = (diff[0] >= cut) | (diff[1] >= cut) | (diff[2] >= cut) | (diff[3] >= cut);
+    const bool any = !((diff[0] < cut) & (diff[1] < cut) & (diff[2] < cut) & (diff[3] < cut));
     if (any) {
       double y[4];
       bool fix = false;
@@ -491,7 +539,7 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
           if (div_needs_ieee(diff[u])) y[u] = __ddiv_rn(diff[u], delta);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) w[u] = (diff[u] >= cut) ? TRSTMI_EXP(y[u]) : 0.0;
+      for (int u = 0; u < 4; ++u) w[u] = (diff[u] < cut) ? 0.0 : TRSTMI_EXP(y[u]);
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u) w[u] = 0.0;
@@ -670,7 +718,7 @@ __device__ int eval_cta(const Prob& P, const double* __restrict__ x, const doubl
 // normalize, else coherence(frame).  |G| = sqrt(re*re + im*im) (CAS).
 // Returns -1 or the first zero column.  Leaves phiS holding the normalised
 // frame (component-major).
-template <bool CPLX, int DMAX, bool EXACT, int S>
+template <bool CPLX, int DMAX, bool EXACT, int S, bool GS = false>
 __device__ int coherence_cta(const Prob& P, const double* __restrict__ f, bool normalize, const Smem& sm, int& rbuf,
                              double* mu_out, long long* arg_out) {
   constexpr int C = CPLX ? 2 : 1;
@@ -698,7 +746,7 @@ __device__ int coherence_cta(const Prob& P, const double* __restrict__ f, bool n
   if (zc != INT_MAX) return zc;
   double best = 0.0;
   long long arg = LLONG_MAX;
-  pairs4<S, true>(P.n, sm.jk, [&](const int* p, const int* j, const int* k, const bool* v) {
+  pairs4<S, true, GS>(P.n, sm.jk, [&](const int* p, const int* j, const int* k, const bool* v) {
     double re[4], im[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) gram_jk<CPLX, DMAX, EXACT>(sm.phiS, N, d, j[u], k[u], re[u], im[u]);

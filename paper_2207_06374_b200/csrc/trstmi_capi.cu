@@ -82,25 +82,70 @@ struct trstmi_ctx {
 };
 
 // ------------------------------------------------------------------ path rule
-static int small_lanes(int field, long long d, long long N) {
-  const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
-  if (dim <= 64) return 32;
-  if (dim <= 256) return 128;
-  return 256;
+// Small-frame kernel choice for a shape: CTA width S (= the CAS reduction
+// width) and pair layout.  Candidates in order; the first whose anneal
+// shared memory fits one SM (227 KB) wins, none -> the large-frame path.
+//   dim <= 64      S = 32   stored Gram (padded / unpadded)
+//   dim <= 256     S = 128  stored Gram, else Gram recomputed
+//   larger         S = 512  stored Gram when even S = 256 leaves one CTA per
+//                           SM (16 warps instead of 8), else S = 256 stored
+//                           Gram, else recomputed
+struct SmallMode {
+  bool ok;
+  int S, gs, pad;
+};
+
+static long long small_bytes(int field, long long d, long long N, int S, int gs, int pad) {
+  const Prob P = make_small_prob(field == TRSTMI_COMPLEX, (int)d, (int)N, kchunks_for((int)d, (int)N, S), gs, pad);
+  return anneal_smem_doubles(P, S, field == TRSTMI_COMPLEX) * 8;
 }
 
-static bool small_fits(int field, long long d, long long N) {
-  if (d > 16 || N > 4096) return false;
-  const int S = small_lanes(field, d, N);
-  Prob P;
-  P.d = (int)d;
-  P.N = (int)N;
-  P.L = (field == TRSTMI_COMPLEX ? 2 : 1) * (int)d;
-  P.dim = P.L * P.N;
-  P.n = (int)(N * (N - 1) / 2);
-  P.K = kchunks_for(P.d, P.N, S);
-  return anneal_smem_doubles(P, S, field == TRSTMI_COMPLEX) * 8 <= 227LL * 1024;
+static SmallMode small_mode(int field, long long d, long long N) {
+  SmallMode m{false, 0, 0, 0};
+  if (d > 16 || N > 4096) return m;
+  const long long dim = (field == TRSTMI_COMPLEX ? 2 : 1) * d * N;
+  const long long kMax = 227LL * 1024;
+  const bool gs_ok = N <= 256 && gs_phys_slots((int)N, 1) <= 65536;  // packed pair table limits
+  int cand[8][3];
+  int nc = 0;
+  auto add = [&](int S, int gs, int pad) {
+    if (gs && !gs_ok) return;
+    cand[nc][0] = S;
+    cand[nc][1] = gs;
+    cand[nc][2] = pad;
+    ++nc;
+  };
+  if (dim <= 64) {
+    add(32, 1, 1);
+    add(32, 1, 0);
+  } else if (dim <= 256) {
+    add(128, 1, 1);
+    add(128, 1, 0);
+    add(128, 0, 0);
+  } else {
+    if (gs_ok && small_bytes(field, d, N, 256, 1, 1) > kMax / 2) {
+      add(512, 1, 1);
+      add(512, 1, 0);
+    }
+    add(256, 1, 1);
+    add(256, 1, 0);
+    add(256, 0, 0);
+  }
+  for (int i = 0; i < nc; ++i) {
+    if (small_bytes(field, d, N, cand[i][0], cand[i][1], cand[i][2]) <= kMax) {
+      m.ok = true;
+      m.S = cand[i][0];
+      m.gs = cand[i][1];
+      m.pad = cand[i][2];
+      return m;
+    }
+  }
+  return m;
 }
+
+static int small_lanes(int field, long long d, long long N) { return small_mode(field, d, N).S; }
+
+static bool small_fits(int field, long long d, long long N) { return small_mode(field, d, N).ok; }
 
 bool trstmi_large::use_large(int field, long long d, long long N) { return !small_fits(field, d, N); }
 
@@ -118,14 +163,13 @@ int fail(trstmi_ctx* ctx, int code, const std::string& msg) {
   } while (0)
 
 Prob make_prob(int field, long long d, long long N) {
-  Prob P;
-  P.d = (int)d;
-  P.N = (int)N;
-  P.L = (field == TRSTMI_COMPLEX ? 2 : 1) * (int)d;
-  P.dim = P.L * P.N;
-  P.n = (int)(N * (N - 1) / 2);
-  P.K = kchunks_for(P.d, P.N, trstmi_lanes(field, d, N));
-  return P;
+  const SmallMode m = small_mode(field, d, N);
+  if (!m.ok) {  // large path shapes: the fields the host code reads
+    Prob P = make_small_prob(field == TRSTMI_COMPLEX, (int)d, (int)N, 1, 0, 0);
+    P.K = kchunks_for(P.d, P.N, trstmi_lanes(field, d, N));
+    return P;
+  }
+  return make_small_prob(field == TRSTMI_COMPLEX, (int)d, (int)N, kchunks_for((int)d, (int)N, m.S), m.gs, m.pad);
 }
 
 int check_shape(trstmi_ctx* ctx, int field, long long d, long long N, const char* who) {
@@ -185,11 +229,13 @@ int trstmi_selftest_cas_math(trstmi_ctx* ctx, int which, const double* x, double
   DBuf dx, dy;
   CUDA_TRY(ctx, cudaMalloc(&dx.p, std::max<int64_t>(n, 1) * 8));
   CUDA_TRY(ctx, cudaMalloc(&dy.p, std::max<int64_t>(n, 1) * 8));
-  CUDA_TRY(ctx, cudaMemcpy(dx.p, x, n * 8, cudaMemcpyHostToDevice));
+  // every copy on the context's (non-blocking) stream: a legacy-stream
+  // cudaMemcpy is not ordered with it and may still be in flight
+  CUDA_TRY(ctx, cudaMemcpyAsync(dx.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
   cas_math_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>((const double*)dx.p, (double*)dy.p, n, which);
   CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaMemcpyAsync(y, dy.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpy(y, dy.p, n * 8, cudaMemcpyDeviceToHost));
   return TRSTMI_OK;
 }
 
@@ -198,11 +244,11 @@ int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t
   cudaSetDevice(ctx->device);
   DBuf db;
   CUDA_TRY(ctx, cudaMalloc(&db.p, 8));
-  CUDA_TRY(ctx, cudaMemset(db.p, 0, 8));
+  CUDA_TRY(ctx, cudaMemsetAsync(db.p, 0, 8, ctx->stream));
   div_selftest_kernel<<<ctx->sm_count * 8, 256, 0, ctx->stream>>>(n, seed, (unsigned long long*)db.p);
   CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaMemcpyAsync(mismatches, db.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaMemcpy(mismatches, db.p, 8, cudaMemcpyDeviceToHost));
   return TRSTMI_OK;
 }
 
@@ -316,7 +362,7 @@ static trstmi_large::Engine* large_engine(trstmi_ctx* ctx, cudaStream_t st) {
 // ------------------------------------------------------------------ eval / hvp / coherence
 static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t N, BatchArgs& A, cudaStream_t st) {
   const int S = trstmi_lanes(field, d, N);
-  const KernelSet* ks = find_kernels(field == TRSTMI_COMPLEX, (int)d, S);
+  const KernelSet* ks = find_kernels(field == TRSTMI_COMPLEX, (int)d, S, A.P.gs);
   if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
   const void* fn = kind == 0 ? ks->eval : kind == 1 ? ks->hvp : ks->coherence;
   const long long dbl = smem_doubles(A.P, S, field == TRSTMI_COMPLEX, kind == 2 ? 0 : 3);
@@ -554,7 +600,7 @@ static int resolve_cfg(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, std:
 
 static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cudaStream_t st) {
   const int S = trstmi_lanes(c->field, c->d, c->N);
-  const KernelSet* ks = find_kernels(c->field == TRSTMI_COMPLEX, c->d, S);
+  const KernelSet* ks = find_kernels(c->field == TRSTMI_COMPLEX, c->d, S, A.P.gs);
   if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
   const size_t bytes = (size_t)anneal_smem_doubles(A.P, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "trial state exceeds one SM's shared memory");
@@ -664,7 +710,8 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
     for (int64_t t = 0; t < trials; ++t) {
       if (to[t].status != TRSTMI_TRIAL_NEED_RESCUE) continue;
       std::vector<double> p(dim);
-      CUDA_TRY(ctx, cudaMemcpy(p.data(), params_dev + t * dim, dim * sizeof(double), cudaMemcpyDeviceToHost));
+      CUDA_TRY(ctx, cudaMemcpyAsync(p.data(), params_dev + t * dim, dim * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(ctx, cudaStreamSynchronize(st));
       int bad;
       if (rng_state) {
         trstmi_host::SplitMix64 rng = trstmi_host::SplitMix64::load(rng_state + 3 * t);
@@ -676,10 +723,12 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
       if (bad >= 0) {  // ZeroColumnError escapes anneal: the restart fails
         to[t].status = TRSTMI_TRIAL_ZERO_COLUMN;
         to[t].zero_col = bad;
-        CUDA_TRY(ctx, cudaMemcpy(trial_out_dev + t, &to[t], sizeof(trstmi_trial_out), cudaMemcpyHostToDevice));
+        CUDA_TRY(ctx, cudaMemcpyAsync(trial_out_dev + t, &to[t], sizeof(trstmi_trial_out), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(ctx, cudaStreamSynchronize(st));
         continue;
       }
-      CUDA_TRY(ctx, cudaMemcpy(params_dev + t * dim, p.data(), dim * sizeof(double), cudaMemcpyHostToDevice));
+      CUDA_TRY(ctx, cudaMemcpyAsync(params_dev + t * dim, p.data(), dim * sizeof(double), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(ctx, cudaStreamSynchronize(st));
       list.push_back((int)t);
       start[t] = to[t].fail_stage;
     }
@@ -688,8 +737,9 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
     DBuf dl, ds;
     CUDA_TRY(ctx, cudaMalloc(&dl.p, list.size() * sizeof(int)));
     CUDA_TRY(ctx, cudaMalloc(&ds.p, trials * sizeof(int)));
-    CUDA_TRY(ctx, cudaMemcpy(dl.p, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CUDA_TRY(ctx, cudaMemcpy(ds.p, start.data(), trials * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(ctx, cudaMemcpyAsync(dl.p, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ds.p, start.data(), trials * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
     A.list = (const int*)dl.p;
     A.start_stage = (const int*)ds.p;
     A.n_list = (int)list.size();
