@@ -192,26 +192,46 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
   const bool chk = !(s >= 0x1.0p-800);
   double zl = 0.0;
   int nnz = 0, tiny = 0;
-#pragma unroll 2
-  for (int p = tid; p < n; p += S) {
-    const unsigned t = tab[p];
-    const int ph = (int)(t & 0xffffu);
-    const double diff = __dsub_rn(U[ph], s);
-    double w = 0.0;
-    if (!(diff < cut)) {  // |y| <= 746 (+1 ulp): the core domain; NaN propagates like cas_exp
-      double y = div_fast(diff, delta, ydelta);
-      if (chk && diff < 0.0 && diff > -0x1.0p-900) y = ieee_div(diff, delta);
-      w = TRSTMI_EXP_CORE(y);
-      ++nnz;                      // an upper bound on the nonzero count: only picks the gradient loop
-      tiny |= (y < -620.0);       // w may be < 2^-900: phase 4 checks its quotients
+  // two pairs (p, p + S) per step inside ONE conditional region, so their
+  // exp chains interleave (a branch per pair serialises them)
+  for (int p = tid; p < n; p += 2 * S) {
+    const int p2 = p + S;
+    const bool v2 = p2 < n;
+    const unsigned t1 = tab[p], t2 = tab[v2 ? p2 : p];
+    const int ph1 = (int)(t1 & 0xffffu), ph2 = (int)(t2 & 0xffffu);
+    const double d1 = __dsub_rn(U[ph1], s), d2 = __dsub_rn(U[ph2], s);
+    const bool k1 = !(d1 < cut), k2 = v2 && !(d2 < cut);  // NaN propagates like cas_exp
+    double w1 = 0.0, w2 = 0.0;
+    if (k1 | k2) {
+      double y1 = div_fast(d1, delta, ydelta), y2 = div_fast(d2, delta, ydelta);
+      if (chk) {
+        if (d1 < 0.0 && d1 > -0x1.0p-900) y1 = ieee_div(d1, delta);
+        if (d2 < 0.0 && d2 > -0x1.0p-900) y2 = ieee_div(d2, delta);
+      }
+      const double e1 = TRSTMI_EXP_CORE(y1), e2 = TRSTMI_EXP_CORE(y2);  // |y| <= 746 (+1 ulp) where taken
+      w1 = k1 ? e1 : 0.0;
+      w2 = k2 ? e2 : 0.0;
+      nnz += (int)k1 + (int)k2;                           // upper bound: only picks the gradient loop
+      tiny |= (k1 && y1 < -620.0) | (k2 && y2 < -620.0);  // w may be < 2^-900: phase 4 checks its quotients
       if (build_mask) {
-        const int j = (int)((t >> 16) & 0xffu), k = (int)(t >> 24);
-        atomicOr(&sm.mask[j * NW + (k >> 5)], 1u << (k & 31));
-        atomicOr(&sm.mask[k * NW + (j >> 5)], 1u << (j & 31));
+        if (k1) {
+          const int j = (int)((t1 >> 16) & 0xffu), k = (int)(t1 >> 24);
+          atomicOr(&sm.mask[j * NW + (k >> 5)], 1u << (k & 31));
+          atomicOr(&sm.mask[k * NW + (j >> 5)], 1u << (j & 31));
+        }
+        if (k2) {
+          const int j = (int)((t2 >> 16) & 0xffu), k = (int)(t2 >> 24);
+          atomicOr(&sm.mask[j * NW + (k >> 5)], 1u << (k & 31));
+          atomicOr(&sm.mask[k * NW + (j >> 5)], 1u << (j & 31));
+        }
       }
     }
-    U[ph] = w;
-    zl = __dadd_rn(zl, w);
+    U[ph1] = w1;
+    zl = __dadd_rn(zl, w1);  // CAS lane order: p, then p + S
+    if (v2) {
+      U[ph2] = w2;
+      zl = __dadd_rn(zl, w2);
+    }
   }
   double zz[3] = {zl, (double)nnz, (double)tiny};
   block_sum<S, 3>(zz, sm.red, rbuf);
@@ -230,7 +250,6 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
     }
   }
   PHASE_MARK(3);
-  PHASE_MARK(4);
 
   // ---- phase 4: gradient (smoothing.hpp:130-160), CAS chunked order.
   // Thread (chunk ch, column m), ascending k in [ch*N/K, (ch+1)*N/K):
@@ -317,6 +336,7 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
     sm.scal[3] = sparse ? 1.0 : 0.0;  // mask prediction for the next evaluation
   }
   __syncthreads();
+  PHASE_MARK(4);
   for (int mq = tid; mq < N * L; mq += S) {
     const int m = mq / L;
     const int q = mq - m * L;

@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
   cudaLaunchKernel(fn, dim3(B), dim3(SS), args, bytes, 0);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long c[8]; cudaMemcpyFromSymbol(c, g_phase_cycles, sizeof(c));
-  const char* names[6] = {"normalize", "gram+max", "exp", "zsum", "coef", "gradient"};
+  const char* names[6] = {"normalize", "gram+max", "exp", "zsum", "grad-loop", "combine"};
   unsigned long long tot = 0; for (int i = 0; i < 6; ++i) tot += c[i];
   printf("%s field=%d d=%d N=%d delta=%g S=%d gs=%d pad=%d smem=%zu: total %.0f cycles/eval\n", cudaGetErrorString(e), field, d, N, delta, SS, GSM, PADM, bytes, tot / (double)B);
   for (int i = 0; i < 6; ++i) printf("  %-10s %8.0f\n", names[i], c[i] / (double)B);
