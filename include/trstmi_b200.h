@@ -173,6 +173,10 @@ int trstmi_set_shard(trstmi_ctx* ctx, int world, int rank, const char* nccl_id);
 int trstmi_lanes(int field, int64_t d, int64_t N);
 /* CAS gradient k-chunk count K for a shape. */
 int trstmi_kchunks(int field, int64_t d, int64_t N);
+/* Kernel layout chosen for a shape (does not change any result bit):
+ * -1 large-frame path, 0 small path with the Gram recomputed in the
+ * gradient, 1 small path with stored Gram, 2 stored Gram in bank-padded rows. */
+int trstmi_small_layout(int field, int64_t d, int64_t N);
 /* Fills cfg with the reference defaults (trust_region.hpp:20-30, solver.hpp:21-29). */
 void trstmi_cfg_defaults(trstmi_cfg* cfg, int field, int d, int N);
 double trstmi_welch_bound(int64_t d, int64_t N);

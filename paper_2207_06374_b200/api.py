@@ -61,6 +61,7 @@ def load_library():
     lib.trstmi_last_error.argtypes = [vp]
     lib.trstmi_last_error.restype = ctypes.c_char_p
     lib.trstmi_lanes.argtypes = [c_int, c_i64, c_i64]
+    lib.trstmi_small_layout.argtypes = [c_int, c_i64, c_i64]
     lib.trstmi_welch_bound.argtypes = [c_i64, c_i64]
     lib.trstmi_welch_bound.restype = c_dbl
     lib.trstmi_default_schedule.argtypes = [c_i64, c_dbl, vp, c_int]
@@ -216,6 +217,12 @@ def default_schedule_len(N, eps_target=1e-7):
 
 def lanes(field, d, N):
     return load_library().trstmi_lanes(field, d, N)
+
+
+def small_layout(field, d, N):
+    """-1 large-frame path, 0 Gram recomputed, 1 stored Gram, 2 stored Gram in
+    bank-padded rows (trstmi_small_layout; a pure function, no GPU needed)."""
+    return load_library().trstmi_small_layout(field, d, N)
 
 
 def welch_bound(d, N):

@@ -7,6 +7,7 @@
 #include <limits>
 #include <atomic>
 #include <map>
+#include <mutex>
 
 #include <nccl.h>
 
@@ -192,6 +193,45 @@ static LargeEval make_eval_w(Work& w, const Shape& sh, const double* x, const do
   return L;
 }
 
+// K1 with its staging buffer (norm_smem(L) bytes of dynamic shared memory)
+static cudaError_t launch_normalize(const LargeEval& L, cudaStream_t st) {
+  const size_t bytes = norm_smem(L.L);
+  static size_t set = 0;  // largest opt-in so far (the attribute is per function, not per stream)
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (bytes > set) {
+      const cudaError_t e = cudaFuncSetAttribute(large_normalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return e;
+      set = bytes;
+    }
+  }
+  const int nc = norm_cols(L.L);
+  large_normalize<<<(L.N + nc - 1) / nc, NORM_THREADS, bytes, st>>>(L);
+  return cudaGetLastError();
+}
+
+// K6 with its two cp.async pipeline buffers (GG_SMEM bytes, > 48 KB opt-in)
+template <bool CPLX>
+static cudaError_t launch_grad_gemm(const LargeEval& L, int cols, int d, int K, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(large_grad_gemm<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GG_SMEM);
+  });
+  if (attr != cudaSuccess) return attr;
+  dim3 gg((cols + GM - 1) / GM, (d + GRB - 1) / GRB, K);
+  large_grad_gemm<CPLX><<<gg, 256, GG_SMEM, st>>>(L);
+  return cudaGetLastError();
+}
+
+// K5 over the upper-triangular pair tiles
+template <bool CPLX>
+static void launch_coef(const LargeEval& L, cudaStream_t st) {
+  const int nt = (L.N + GT - 1) / GT;
+  large_coef<CPLX><<<nt * (nt + 1) / 2, 256, 0, st>>>(L);
+}
+
 static LargeEval make_eval(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta,
                            int squared, double* grad, double* weights) {
   return make_eval_w(E->w, sh, x, dir, sc, delta, squared, grad, weights);
@@ -209,7 +249,7 @@ int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double 
   cudaStream_t st = E->st;
   LargeEval L = make_eval(E, sh, x, dir, sc, delta, squared, grad, weights);
   LCHK(cudaMemsetAsync(w.zero_col, 0x7f, 4, st));
-  large_normalize<<<(sh.N + 127) / 128, 128, 0, st>>>(L);
+  LCHK(launch_normalize(L, st));
   const int nt = (sh.N + GT - 1) / GT;
   const int tiles = nt * (nt + 1) / 2;
   if (sh.cplx) large_gram<true, 0><<<tiles, 256, 0, st>>>(L, nullptr, nullptr);
@@ -217,16 +257,12 @@ int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double 
   const int nzb = (sh.N + ZROWS - 1) / ZROWS;
   large_weights<<<nzb, ZLANES, 0, st>>>(L);
   large_zreduce<<<1, 32, 0, st>>>(L, nzb);
-  const int cblocks = (int)std::min<long long>((sh.n + 255) / 256, 148LL * 16);
-  if (sh.cplx) large_coef<true><<<std::max(cblocks, 1), 256, 0, st>>>(L);
-  else large_coef<false><<<std::max(cblocks, 1), 256, 0, st>>>(L);
-  const int RB = sh.cplx ? 32 : 64;
-  dim3 gg((sh.N + GM - 1) / GM, (sh.d + RB - 1) / RB, sh.K);
-  if (sh.cplx) large_grad_gemm<true><<<gg, 256, 0, st>>>(L);
-  else large_grad_gemm<false><<<gg, 256, 0, st>>>(L);
-  large_tsum<<<dim3((sh.N + 127) / 128, sh.K), 128, 0, st>>>(L);
+  if (sh.cplx) launch_coef<true>(L, st);
+  else launch_coef<false>(L, st);
+  if (sh.cplx) LCHK(launch_grad_gemm<true>(L, sh.N, sh.d, sh.K, st));
+  else LCHK(launch_grad_gemm<false>(L, sh.N, sh.d, sh.K, st));
   large_finalize<<<(sh.dim + 255) / 256, 256, 0, st>>>(L);
-  g_large_launches += 9;
+  g_large_launches += 8;
   LCHK(cudaGetLastError());
   LCHK(cudaMemcpyAsync(E->h_scal, w.scal, 3 * 8, cudaMemcpyDeviceToHost, st));
   LCHK(cudaMemcpyAsync(E->h_scal + 4, w.zero_col, 4, cudaMemcpyDeviceToHost, st));
@@ -297,7 +333,7 @@ static int eval_sharded(Engine* E, const Shape& sh, const double* x, const doubl
   // phase A: normalise, Gram of the shard's tiles, local max
   for (int r : ranks) {
     LCHK(cudaMemsetAsync(work(r).zero_col, 0x7f, 4, st));
-    large_normalize<<<(sh.N + 127) / 128, 128, 0, st>>>(Ls[r]);
+    LCHK(launch_normalize(Ls[r], st));
     if (sh.cplx) large_gram<true, 0><<<tiles, 256, 0, st>>>(Ls[r], nullptr, nullptr);
     else large_gram<false, 0><<<tiles, 256, 0, st>>>(Ls[r], nullptr, nullptr);
   }
@@ -343,24 +379,20 @@ static int eval_sharded(Engine* E, const Shape& sh, const double* x, const doubl
     NCHK(ncclGroupEnd());
   }
   // phase C: z, coefficients, gradient columns of the shard
-  const int RB = sh.cplx ? 32 : 64;
   for (int r : ranks) {
     const LargeEval& L = Ls[r];
     large_zreduce<<<1, 32, 0, st>>>(L, nzb);
-    const int cblocks = (int)std::min<long long>((sh.n + 255) / 256, 148LL * 16);
-    if (sh.cplx) large_coef<true><<<std::max(cblocks, 1), 256, 0, st>>>(L);
-    else large_coef<false><<<std::max(cblocks, 1), 256, 0, st>>>(L);
+    if (sh.cplx) launch_coef<true>(L, st);
+    else launch_coef<false>(L, st);
     const int cols = L.m1 - L.m0;
     if (cols > 0) {
-      dim3 gg((cols + GM - 1) / GM, (sh.d + RB - 1) / RB, sh.K);
-      if (sh.cplx) large_grad_gemm<true><<<gg, 256, 0, st>>>(L);
-      else large_grad_gemm<false><<<gg, 256, 0, st>>>(L);
-      large_tsum<<<dim3((cols + 127) / 128, sh.K), 128, 0, st>>>(L);
+      if (sh.cplx) LCHK(launch_grad_gemm<true>(L, cols, sh.d, sh.K, st));
+      else LCHK(launch_grad_gemm<false>(L, cols, sh.d, sh.K, st));
       large_finalize<<<(int)(((long long)cols * sh.L + 255) / 256), 256, 0, st>>>(L);
     }
   }
   LCHK(cudaGetLastError());
-  g_large_launches += (long long)ranks.size() * 9;
+  g_large_launches += (long long)ranks.size() * 8;
   if (!E->virtual_ranks) {  // gradient column slices to every rank
     NCHK(ncclGroupStart());
     for (int r = 0; r < G; ++r) {
@@ -494,7 +526,7 @@ int coherence(Engine* E, const Shape& sh, const double* frame, int normalize, do
   cudaStream_t st = E->st;
   LargeEval L = make_eval(E, sh, frame, nullptr, 0.0, 1.0, 1, nullptr, nullptr);
   LCHK(cudaMemsetAsync(w.zero_col, 0x7f, 4, st));
-  if (normalize) large_normalize<<<(sh.N + 127) / 128, 128, 0, st>>>(L);
+  if (normalize) LCHK(launch_normalize(L, st));
   std::vector<double> hframe;
   if (!normalize) {
     hframe.resize(sh.dim);

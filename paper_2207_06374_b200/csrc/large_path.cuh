@@ -9,7 +9,7 @@
 //   K4 large_zreduce     z = block partials in row order; F = s + delta log z
 //   K5 large_coef        c = w/z; dense coefficient matrices P = c G (k,m) and c u
 //   K6 large_grad_gemm   chunked D = Phi P (register-tiled DGEMM, CAS k-chunks)
-//   K6b large_tsum       t chunk partials
+//                        and, in its rb == 0 CTAs, the t chunk partials
 //   K7 large_finalize    chunk combine, grad = ((acc - t phi)/alpha) * 2
 //
 // Arithmetic is the Canonical Arithmetic Spec with S = 32768
@@ -59,28 +59,39 @@ struct LargeEval {
   int m0, m1;                      // owned rows / gradient columns [m0, m1) (row-block shard; full = [0, N))
 };
 
-// ---- K1
-__global__ void large_normalize(LargeEval E) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// ---- K1: a CTA normalises NC consecutive columns: the columns' NC*L
+// doubles (one contiguous run of the point) are staged through shared memory
+// with coalesced loads, then thread c runs column c's CAS norm chain
+// (ascending fma) and divides by Markstein quotients (== IEEE division).
+constexpr int NORM_THREADS = 128;
+__host__ __device__ inline int norm_cols(int L) { return max(1, min(128, 6144 / (L + 1))); }
+__host__ __device__ inline size_t norm_smem(int L) { return (size_t)norm_cols(L) * (L + 1) * sizeof(double); }
+__global__ void __launch_bounds__(NORM_THREADS) large_normalize(LargeEval E) {
+  extern __shared__ double ncol[];  // NC x (L + 1)
   if (blockIdx.x == 0 && threadIdx.x == 0) *E.smax_bits = 0ull;
-  if (j >= E.N) return;
-  const int L = E.L;
-  double acc = 0.0;
-  for (int q = 0; q < L; ++q) {
-    const double xv = E.x[(long long)j * L + q];
-    const double pv = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[(long long)j * L + q]));
-    acc = fma(pv, pv, acc);
+  const int L = E.L, LP = L + 1, NC = norm_cols(L);
+  const int j0 = blockIdx.x * NC;
+  const int nc = min(NC, E.N - j0);
+  const long long base = (long long)j0 * L;
+  for (int e = threadIdx.x; e < nc * L; e += NORM_THREADS) {
+    const int c = e / L, q = e - c * L;
+    const double xv = E.x[base + e];
+    ncol[c * LP + q] = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[base + e]));
   }
-  const double a = sqrt(acc);
-  E.alpha[j] = a;
-  if (a < kZeroColumnTol) {
-    atomicMin(E.zero_col, j);
-    return;
-  }
-  for (int q = 0; q < L; ++q) {
-    const double xv = E.x[(long long)j * L + q];
-    const double pv = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[(long long)j * L + q]));
-    E.phiT[(long long)q * E.N + j] = __ddiv_rn(pv, a);
+  __syncthreads();
+  for (int c = threadIdx.x; c < nc; c += NORM_THREADS) {
+    const double* col = ncol + c * LP;
+    const int j = j0 + c;
+    double acc = 0.0;
+    for (int q = 0; q < L; ++q) acc = fma(col[q], col[q], acc);
+    const double a = sqrt(acc);
+    E.alpha[j] = a;
+    if (a < kZeroColumnTol) {
+      atomicMin(E.zero_col, j);
+      continue;
+    }
+    const double ya = __drcp_rn(a);
+    for (int q = 0; q < L; ++q) E.phiT[(long long)q * E.N + j] = div_rn(col[q], a, ya);
   }
 }
 
@@ -240,12 +251,31 @@ __global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
     return;
   }
   const long long p0 = r0 * N - r0 * (r0 + 1) / 2, p1 = r1 * N - r1 * (r1 + 1) / 2;
+  const double yd = __drcp_rn(E.delta);
+  const bool chk = !(s >= 0x1.0p-800);  // else every nonzero |x - s| >= 2^-854 (Markstein exact)
+  double* __restrict__ X = E.X;
   double zp = 0.0;
-  for (long long p = p0 + threadIdx.x; p < p1; p += ZLANES) {
-    const double diff = __dsub_rn(E.X[p], s);
-    const double w = (diff < cut) ? 0.0 : cas_exp(__ddiv_rn(diff, E.delta));
-    E.X[p] = w;
-    zp = __dadd_rn(zp, w);
+  // four independent pairs per step (lane order l, l+256, l+512, l+768 is
+  // also the CAS z order), all loads issued before the stores
+  for (long long p = p0 + threadIdx.x; p < p1; p += 4 * ZLANES) {
+    double xv[4], w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = (p + u * ZLANES < p1) ? X[p + u * ZLANES] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double diff = __dsub_rn(xv[u], s);
+      double y = div_fast(diff, E.delta, yd);
+      if (chk && diff < 0.0 && diff > -0x1.0p-900) y = __ddiv_rn(diff, E.delta);
+      const double e = cas_exp_core(y);  // the core domain wherever !(diff < cut)
+      w[u] = (diff < cut) ? 0.0 : e;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (p + u * ZLANES < p1) {
+        X[p + u * ZLANES] = w[u];
+        zp = __dadd_rn(zp, w[u]);
+      }
+    }
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) zp = __dadd_rn(zp, __shfl_xor_sync(FULL, zp, off));
@@ -270,95 +300,164 @@ __global__ void large_zreduce(LargeEval E, int nblocks) {
   E.scal[2] = __dadd_rn(E.scal[0], __dmul_rn(E.delta, cas_log(z)));
 }
 
-// ---- K5: coefficients into dense P (row k, column m): P(k,m) = c G(k,m)
+// ---- K5: coefficients into dense P (row k, column m): P(k,m) = c G(k,m),
+// one CTA per upper-triangular 64x64 pair tile: the packed rows are read
+// coalesced, P(j,k) written row-major and P(k,j) through a shared-memory
+// transpose (both coalesced).  c = w / z by Markstein quotients (== IEEE).
 template <bool CPLX>
-__global__ void large_coef(LargeEval E) {
-  const double z = E.scal[1];
+__global__ void __launch_bounds__(256) large_coef(LargeEval E) {
+  constexpr int HR = 16;  // tile rows per pass (4 elements per thread: few registers, high occupancy)
+  __shared__ double tv[3][HR][GT + 1];
   const int N = E.N;
-  const long long pend = (long long)E.m1 * N - (long long)E.m1 * (E.m1 + 1) / 2;  // rows < m1
-  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pend; p += (long long)gridDim.x * blockDim.x) {
-    // pair -> (j, k)
-    const double b = 2.0 * N - 1.0;
-    long long j = (long long)floor(0.5 * (b - sqrt(fmax(b * b - 8.0 * (double)p, 0.0))));
-    j = max(0LL, min(j, (long long)N - 2));
-    while (j < N - 2 && (j + 1) * N - (j + 1) * (j + 2) / 2 <= p) ++j;
-    while (j > 0 && j * N - j * (j + 1) / 2 > p) --j;
-    const long long k = p - (j * N - j * (j + 1) / 2) + j + 1;
-    if (!(j >= E.m0 || (k >= E.m0 && k < E.m1))) continue;  // shard: rows before m0 only in owned columns
-    const double w = E.X[p];
-    const double c = (w == 0.0) ? 0.0 : __ddiv_rn(w, z);
-    if (E.wout) E.wout[p] = c;
-    const double gr = E.GR[p];
-    const double gi = CPLX ? E.GI[p] : 0.0;
-    const double u = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
-    double cc = c;
-    if (!E.squared && c != 0.0) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(u), 1e-150)));
-    const double cr = c == 0.0 ? 0.0 : __dmul_rn(cc, gr);
-    const double ci = c == 0.0 ? 0.0 : __dmul_rn(cc, gi);
-    const double cu = c == 0.0 ? 0.0 : __dmul_rn(cc, u);
-    E.PR[j * N + k] = cr;
-    E.PR[k * N + j] = cr;
-    E.CU[j * N + k] = cu;
-    E.CU[k * N + j] = cu;
-    if (CPLX) {
-      E.PI[j * N + k] = ci;
-      E.PI[k * N + j] = -ci;
+  const int nt = (N + GT - 1) / GT;
+  int jb, kb;
+  tile_of(blockIdx.x, nt, jb, kb);
+  if (jb * GT >= E.m1) return;  // rows >= m1 are not owned
+  const double z = E.scal[1];
+  const double yz = __drcp_rn(z);
+  for (int h = 0; h < GT; h += HR) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < HR * GT / 256; ++i) {
+      const int e = threadIdx.x + 256 * i;
+      const int r = e / GT, c = e - r * GT;
+      const int j = jb * GT + h + r, k = kb * GT + c;
+      // shard: rows >= m0, plus the owned columns of the rows before m0
+      const bool ok = j < k && k < N && j < E.m1 && (j >= E.m0 || (k >= E.m0 && k < E.m1));
+      double vr = 0.0, vi = 0.0, vu = 0.0;
+      if (ok) {
+        const long long p = (long long)j * N - (long long)j * (j + 1) / 2 + (k - j - 1);
+        const double w = E.X[p];
+        const double cq = (w == 0.0) ? 0.0 : div_rn(w, z, yz);
+        if (E.wout) E.wout[p] = cq;
+        if (cq != 0.0) {
+          const double gr = E.GR[p];
+          const double gi = CPLX ? E.GI[p] : 0.0;
+          const double u = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+          double cc = cq;
+          if (!E.squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(u), 1e-150)));
+          vr = __dmul_rn(cc, gr);
+          vi = __dmul_rn(cc, gi);
+          vu = __dmul_rn(cc, u);
+        }
+        const long long o = (long long)j * N + k;
+        E.PR[o] = vr;
+        E.CU[o] = vu;
+        if (CPLX) E.PI[o] = vi;
+      }
+      tv[0][r][c] = vr;
+      tv[1][r][c] = vu;
+      tv[2][r][c] = -vi;  // P(k,j) = c conj(G(j,k))
+    }
+    __syncthreads();
+    // transposed: row k = kb*GT + c2 (64 rows), columns j = jb*GT + h + r2 (16 per row)
+#pragma unroll
+    for (int i = 0; i < HR * GT / 256; ++i) {
+      const int e = threadIdx.x + 256 * i;
+      const int c2 = e / HR, r2 = e - c2 * HR;
+      const int j = jb * GT + h + r2, k = kb * GT + c2;
+      const bool ok = j < k && k < N && j < E.m1 && (j >= E.m0 || (k >= E.m0 && k < E.m1));
+      if (ok) {
+        const long long o = (long long)k * N + j;
+        E.PR[o] = tv[0][r2][c2];
+        E.CU[o] = tv[1][r2][c2];
+        if (CPLX) E.PI[o] = tv[2][r2][c2];
+      }
     }
   }
 }
 
 // ---- K6: chunked gradient GEMM D(q, m) = sum_k phi(q, k) (x) P(k, m)
-// over k in chunk c (ascending), register tile 4 m x RT rows per thread.
-constexpr int GM = 64, GK = 16;
+// over k in chunk c (ascending), register tile 4 m x 4 rows per thread.
+// Operand tiles stream global -> shared with cp.async into two buffers, so
+// the next k-step's loads overlap this step's FMAs.  The rb == 0 CTAs also
+// sum the c*u tile into the t chunk partials (ascending k, add).
+constexpr int GM = 64, GK = 16, GRB = 64;  // columns, k-step, rows per CTA
+constexpr int GG_BUF = GK * GM * 3 + GK * GRB * 2;  // doubles per pipeline buffer
+constexpr size_t GG_SMEM = 2 * GG_BUF * sizeof(double);
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
+
 template <bool CPLX>
 __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
-  constexpr int RT = CPLX ? 2 : 4;          // complex rows / real rows per thread
-  constexpr int RB = 16 * RT;               // rows per tile (complex rows or real rows)
-  __shared__ double sPr[GK][GM], sPi[GK][GM];
-  __shared__ double sFr[GK][RB], sFi[GK][RB];
+  constexpr int RT = 4;  // complex rows / real rows per thread
+  extern __shared__ double gsm[];
   const int N = E.N, d = E.d, K = E.K;
   const int mb = blockIdx.x + E.m0 / GM, rb = blockIdx.y, ch = blockIdx.z;
   const int k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
   const int tid = threadIdx.x;
   const int tm = tid & 15, tr = tid >> 4;
+  const bool tsum = rb == 0 && tr == 0;  // threads 0..15: t of columns tm + 16c, ascending k (c*u add)
+  auto issue = [&](int k0, int b) {
+    double* base = gsm + b * GG_BUF;
+    for (int e = tid; e < GK * GM; e += 256) {
+      const int kk = e / GM, c = e - kk * GM;
+      const int k = k0 + kk, m = mb * GM + c;
+      const bool v = k < k_hi && m < E.m1;
+      const long long o = v ? (long long)k * N + m : 0;
+      cp_async8(base + e, E.PR + o, v);
+      if (CPLX) cp_async8(base + GK * GM + e, E.PI + o, v);
+      if (rb == 0) cp_async8(base + 2 * GK * GM + e, E.CU + o, v);
+    }
+    for (int e = tid; e < GK * GRB; e += 256) {  // lanes along k: 128-byte runs of phi rows
+      const int kk = e % GK, r = e / GK;
+      const int k = k0 + kk, row = rb * GRB + r;
+      const bool v = k < k_hi && row < d;
+      double* dst = base + 3 * GK * GM + kk * GRB + r;
+      if (CPLX) {
+        cp_async8(dst, E.phiT + (v ? (long long)(2 * row) * N + k : 0), v);
+        cp_async8(dst + GK * GRB, E.phiT + (v ? (long long)(2 * row + 1) * N + k : 0), v);
+      } else {
+        cp_async8(dst, E.phiT + (v ? (long long)row * N + k : 0), v);
+      }
+    }
+    cp_async_commit();
+  };
   double ar[RT][4], ai[RT][4];
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) ar[r][c] = ai[r][c] = 0.0;
-  for (int k0 = k_lo; k0 < k_hi; k0 += GK) {
-    __syncthreads();
-    for (int e = tid; e < GK * GM; e += 256) {
-      const int kk = e / GM, c = e - kk * GM;
-      const int k = k0 + kk, m = mb * GM + c;
-      const bool v = k < k_hi && m < E.m1;
-      sPr[kk][c] = v ? E.PR[(long long)k * N + m] : 0.0;
-      if (CPLX) sPi[kk][c] = v ? E.PI[(long long)k * N + m] : 0.0;
-    }
-    for (int e = tid; e < GK * RB; e += 256) {
-      const int kk = e / RB, r = e - kk * RB;
-      const int k = k0 + kk, row = rb * RB + r;
-      const bool v = k < k_hi && row < d;
-      if (CPLX) {
-        sFr[kk][r] = v ? E.phiT[(long long)(2 * row) * N + k] : 0.0;
-        sFi[kk][r] = v ? E.phiT[(long long)(2 * row + 1) * N + k] : 0.0;
-      } else {
-        sFr[kk][r] = v ? E.phiT[(long long)row * N + k] : 0.0;
-      }
+  double tc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int nsteps = (k_hi - k_lo + GK - 1) / GK;
+  if (nsteps > 0) issue(k_lo, 0);
+  for (int st = 0; st < nsteps; ++st) {
+    const int b = st & 1, k0 = k_lo + st * GK;
+    if (st + 1 < nsteps) {
+      issue(k0 + GK, b ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    const double* sPr = gsm + b * GG_BUF;
+    const double* sPi = sPr + GK * GM;
+    const double* sCU = sPr + 2 * GK * GM;
+    const double* sFr = sPr + 3 * GK * GM;
+    const double* sFi = sFr + GK * GRB;
     const int kmax = min(GK, k_hi - k0);
+    if (tsum) {
+      for (int kk = 0; kk < kmax; ++kk)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc[c] = __dadd_rn(tc[c], sCU[kk * GM + tm + 16 * c]);
+    }
     for (int kk = 0; kk < kmax; ++kk) {
       double pr[4], pi[4], fr[RT], fi[RT];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        pr[c] = sPr[kk][tm + 16 * c];
-        if (CPLX) pi[c] = sPi[kk][tm + 16 * c];
+        pr[c] = sPr[kk * GM + tm + 16 * c];
+        if (CPLX) pi[c] = sPi[kk * GM + tm + 16 * c];
       }
 #pragma unroll
       for (int r = 0; r < RT; ++r) {
-        fr[r] = sFr[kk][tr + 16 * r];
-        if (CPLX) fi[r] = sFi[kk][tr + 16 * r];
+        fr[r] = sFr[kk * GRB + tr + 16 * r];
+        if (CPLX) fi[r] = sFi[kk * GRB + tr + 16 * r];
       }
 #pragma unroll
       for (int r = 0; r < RT; ++r)
@@ -374,12 +473,20 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
           }
         }
     }
+    __syncthreads();  // buffer b is refilled by the issue two steps on
+  }
+  if (tsum) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int m = mb * GM + tm + 16 * c;
+      if (m < E.m1) E.tpart[(long long)ch * N + m] = tc[c];
+    }
   }
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int row = rb * RB + tr + 16 * r, m = mb * GM + tm + 16 * c;
+      const int row = rb * GRB + tr + 16 * r, m = mb * GM + tm + 16 * c;
       if (row < d && m < E.m1) {
         double* out = E.part + (long long)ch * E.dim + (long long)m * E.L;
         if (CPLX) {
@@ -390,18 +497,6 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
         }
       }
     }
-}
-
-// ---- K6b: t chunk partials, thread per (chunk, m), ascending k (c*u add)
-__global__ void large_tsum(LargeEval E) {
-  const int ch = blockIdx.y;
-  const int m = E.m0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= E.m1) return;
-  const int k_lo = (ch * E.N) / E.K, k_hi = ((ch + 1) * E.N) / E.K;
-  double t = 0.0;
-#pragma unroll 16
-  for (int k = k_lo; k < k_hi; ++k) t = __dadd_rn(t, E.CU[(long long)k * E.N + m]);
-  E.tpart[(long long)ch * E.N + m] = t;
 }
 
 // ---- K7: chunk partials added left to right; grad = ((acc - t phi)/alpha)*2

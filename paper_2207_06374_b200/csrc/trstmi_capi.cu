@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -268,6 +269,12 @@ int trstmi_set_shard(trstmi_ctx* ctx, int world, int rank, const char* nccl_id) 
   return rc;
 }
 
+int trstmi_small_layout(int field, int64_t d, int64_t N) {
+  const SmallMode m = small_mode(field, d, N);
+  if (!m.ok) return -1;
+  return m.gs ? 1 + m.pad : 0;
+}
+
 int trstmi_kchunks(int field, int64_t d, int64_t N) { return kchunks_for((int)d, (int)N, trstmi_lanes(field, d, N)); }
 
 int trstmi_lanes(int field, int64_t d, int64_t N) {
@@ -353,6 +360,14 @@ int trstmi_ctx_destroy(trstmi_ctx* ctx) {
 }
 
 const char* trstmi_last_error(const trstmi_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+// concurrent large-path trials (host worker + stream + workspace each);
+// TRSTMI_LARGE_WORKERS overrides the context default
+static int large_workers(const trstmi_ctx* ctx) {
+  const char* e = std::getenv("TRSTMI_LARGE_WORKERS");
+  const int v = e ? std::atoi(e) : 0;
+  return v > 0 ? v : ctx->large_workers;
+}
 
 static trstmi_large::Engine* large_engine(trstmi_ctx* ctx, cudaStream_t st) {
   if (!ctx->large) ctx->large = trstmi_large::engine_create(ctx->device, st);
@@ -645,7 +660,7 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
     // atomic counter; each drives its trial's trust-region loop.
     CUDA_TRY(ctx, cudaStreamSynchronize(st));
     const int workers =
-        ctx->shard_world > 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(trials, ctx->large_workers));
+        ctx->shard_world > 1 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(trials, large_workers(ctx)));
     std::atomic<int64_t> next{0};
     std::vector<int> rcs(workers, TRSTMI_OK);
     std::vector<std::string> errs(workers);
