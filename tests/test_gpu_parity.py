@@ -253,3 +253,36 @@ def test_nonfinite_start_fails_like_the_reference(ctx):
     o = orc.solve_batch(cfg, api.lanes(C, 2, 6), starts, st, threads=2)
     assert g["trials"][0].status == o["trials"][0].status == abi.TRIAL_OK
     assert g["trials"][1].status == o["trials"][1].status
+
+
+# one shape per (kernel layout, CAS width) the dispatcher can pick
+# (trstmi_small_layout: 0 Gram recomputed, 1 stored Gram, 2 stored Gram in
+# bank-padded rows): the same bits whichever layout runs
+LAYOUTS = [(C, 1, 128, 0, 128), (C, 1, 140, 0, 256), (C, 1, 116, 1, 128), (C, 2, 110, 1, 256),
+           (C, 3, 100, 1, 512), (C, 2, 80, 2, 512), (C, 3, 44, 2, 256), (C, 1, 35, 2, 128),
+           (R, 2, 150, 0, 256), (R, 4, 40, 2, 128)]
+
+
+@pytest.mark.parametrize("field,d,N,layout,lanes", LAYOUTS)
+def test_every_layout_bit_exact(ctx, field, d, N, layout, lanes):
+    from paper_2207_06374_b200 import api
+    assert api.small_layout(field, d, N) == layout and api.lanes(field, d, N) == lanes
+    S = lanes
+    pts = frames_for(field, d, N, [21, 22])
+    for delta in (1e-1, 1e-5):
+        F, s, g, w, zc = ctx.eval_batch(field, d, N, pts, delta, True, True)
+        for b in range(pts.shape[0]):
+            Fo, so, go, wo, zo = orc.eval_objective(field, d, N, S, pts[b], delta, want_weights=True)
+            assert bits(F[b]) == bits(Fo) and np.array_equal(bits(g[b]), bits(go))
+            assert np.array_equal(bits(w[b]), bits(wo))
+    dirs = frames_for(field, d, N, [31, 32])
+    hv, path, zc = ctx.hvp_batch(field, d, N, pts, dirs, 1e-3)
+    for b in range(pts.shape[0]):
+        ho, po, zo = orc.hvp(field, d, N, S, pts[b], dirs[b], 1e-3)
+        assert path[b] == po and np.array_equal(bits(hv[b]), bits(ho))
+    cfg = abi.default_cfg(field, d, N, 8)
+    cfg.record_cap = 400
+    starts, st = api.random_frames(field, d, N, 0, 0, 2)
+    gr = ctx.solve_batch(cfg, starts, st)
+    o = orc.solve_batch(cfg, S, starts, st)
+    _cmp_solve(gr, o, 2, gr["n_stages"], 400)
