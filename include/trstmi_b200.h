@@ -238,6 +238,23 @@ int trstmi_solve(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restarts, uint6
                  double* best_frame, double* best_coherence, int64_t* best_restart, trstmi_trial_out* trial_out,
                  trstmi_stage_out* stage_out);
 
+/* Child seed of restart `index` (mix_seed, rng.hpp:13-18): RestartRecord::seed. */
+uint64_t trstmi_mix_seed(uint64_t seed, uint64_t index);
+
+/* ---- post-solve analysis (csrc/analysis.cu).  Host
+ * buffers; run on the default stream and synchronise.  No context needed. */
+/* offdiagonal_magnitudes (frame.hpp:80-91): n = N(N-1)/2 magnitudes |G(j,k)|
+ * in row-major upper-triangular order into mags (nullable); sorted_mags
+ * (nullable) receives them in ascending order (device sort).  normalize != 0
+ * first applies normalize_columns (frame.hpp:60-69): ZERO_COLUMN + *zero_col. */
+int trstmi_offdiag_magnitudes(int field, int64_t d, int64_t N, const double* frame, int normalize, double* mags,
+                              double* sorted_mags, int64_t* zero_col);
+/* cluster_magnitudes (frame.hpp:96-118) over an ascending array: means of the
+ * single-linkage clusters (gap > cluster_tol), sequential sums; *count means. */
+int trstmi_cluster_sorted(const double* sorted, int64_t n, double cluster_tol, double* means, int64_t* count);
+/* check_tight's deviation (analysis.hpp:76-84): max |(Phi Phi*)(r,s) - (N/d) I| */
+int trstmi_frame_operator_deviation(int field, int64_t d, int64_t N, const double* frame, double* deviation);
+
 #ifdef __cplusplus
 }
 #endif

@@ -226,6 +226,19 @@ std::int64_t orc_hvp(int field, std::int64_t d, std::int64_t N, int lanes, const
   return -1;
 }
 
+// offdiagonal_magnitudes (frame.hpp:80-91) of a frame, CAS |G| (the checker
+// of trstmi_offdiag_magnitudes)
+void orc_offdiag_magnitudes(int field, std::int64_t d, std::int64_t N, const double* frame, double* mags) {
+  Shape sh = make_shape(field, d, N, 32);
+  const std::int64_t L = sh.col_len();
+  for (std::int64_t j = 0, p = 0; j < N; ++j)
+    for (std::int64_t k = j + 1; k < N; ++k, ++p) {
+      double gr, gi;
+      gram_entry(sh, frame + j * L, frame + k * L, &gr, &gi);
+      mags[p] = std::sqrt(gr * gr + gi * gi);
+    }
+}
+
 std::int64_t orc_coherence(int field, std::int64_t d, std::int64_t N, const double* frame, int normalize, double* mu,
                            std::int64_t* argmax) {
   Shape sh = make_shape(field, d, N, 32);

@@ -62,6 +62,11 @@ def load_library():
     lib.trstmi_last_error.restype = ctypes.c_char_p
     lib.trstmi_lanes.argtypes = [c_int, c_i64, c_i64]
     lib.trstmi_small_layout.argtypes = [c_int, c_i64, c_i64]
+    lib.trstmi_mix_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+    lib.trstmi_mix_seed.restype = ctypes.c_uint64
+    lib.trstmi_offdiag_magnitudes.argtypes = [c_int, c_i64, c_i64, vp, c_int, vp, vp, vp]
+    lib.trstmi_cluster_sorted.argtypes = [vp, c_i64, c_dbl, vp, vp]
+    lib.trstmi_frame_operator_deviation.argtypes = [c_int, c_i64, c_i64, vp, vp]
     lib.trstmi_welch_bound.argtypes = [c_i64, c_i64]
     lib.trstmi_welch_bound.restype = c_dbl
     lib.trstmi_default_schedule.argtypes = [c_i64, c_dbl, vp, c_int]

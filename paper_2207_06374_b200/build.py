@@ -64,7 +64,7 @@ def build(verbose=False, force=False, jobs=None):
         objs.append(o)
         tasks.append(COMMON + ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-DINST_GS=%d" % g, "-c",
                                os.path.join(CSRC, "instantiate.cu"), "-o", o])
-    for src in ("trstmi_capi.cu", "large_engine.cu"):
+    for src in ("trstmi_capi.cu", "large_engine.cu", "analysis.cu"):
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         tasks.append(COMMON + ["-c", os.path.join(CSRC, src), "-o", o])

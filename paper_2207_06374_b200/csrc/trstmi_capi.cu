@@ -269,6 +269,8 @@ int trstmi_set_shard(trstmi_ctx* ctx, int world, int rank, const char* nccl_id) 
   return rc;
 }
 
+uint64_t trstmi_mix_seed(uint64_t seed, uint64_t index) { return trstmi_host::mix_seed(seed, index); }
+
 int trstmi_small_layout(int field, int64_t d, int64_t N) {
   const SmallMode m = small_mode(field, d, N);
   if (!m.ok) return -1;

@@ -54,6 +54,7 @@ def lib():
         L.orc_hvp.restype = i64
         L.orc_coherence.argtypes = [c_int, i64, i64, vp, c_int, vp, vp]
         L.orc_coherence.restype = i64
+        L.orc_offdiag_magnitudes.argtypes = [c_int, i64, i64, vp, vp]
         L.orc_solve_batch.argtypes = [vp, c_int, i64, vp, vp, vp, vp, vp, vp, c_int]
         L.orc_time_solve_batch.argtypes = [vp, c_int, i64, vp, vp, c_int, vp, vp]
         L.orc_time_solve_batch.restype = dbl
@@ -172,3 +173,14 @@ def solve_batch(cfg, S, params, rng_state=None, threads=8, want_frames=True):
                                ctypes.cast(oo, ctypes.c_void_p) if oo is not None else None, threads)
     assert rc == 0
     return dict(params=params, frames=frames, trials=to, stages=so, outer=oo, n_stages=ns, rng=rng)
+
+
+def offdiag_magnitudes(field, d, N, frame):
+    frame = np.ascontiguousarray(frame, np.float64)
+    out = np.empty(N * (N - 1) // 2)
+    lib().orc_offdiag_magnitudes(field, d, N, _p(frame), _p(out))
+    return out
+
+
+def mix_seed(seed, index):
+    return int(lib().orc_mix_seed(seed, index))
