@@ -249,6 +249,9 @@ uint64_t trstmi_mix_seed(uint64_t seed, uint64_t index);
  * first applies normalize_columns (frame.hpp:60-69): ZERO_COLUMN + *zero_col. */
 int trstmi_offdiag_magnitudes(int field, int64_t d, int64_t N, const double* frame, int normalize, double* mags,
                               double* sorted_mags, int64_t* zero_col);
+/* normalize_columns (frame.hpp:60-69) in place (CAS norm, IEEE-exact division);
+ * ZERO_COLUMN with *zero_col = the first column whose norm is < 1e-12. */
+int trstmi_normalize_columns(int field, int64_t d, int64_t N, double* frame, int64_t* zero_col);
 /* cluster_magnitudes (frame.hpp:96-118) over an ascending array: means of the
  * single-linkage clusters (gap > cluster_tol), sequential sums; *count means. */
 int trstmi_cluster_sorted(const double* sorted, int64_t n, double cluster_tol, double* means, int64_t* count);

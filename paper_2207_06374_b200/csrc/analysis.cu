@@ -166,6 +166,16 @@ int trstmi_offdiag_magnitudes(int field, int64_t d, int64_t N, const double* fra
   return cudaDeviceSynchronize() == cudaSuccess ? TRSTMI_OK : TRSTMI_ERR_CUDA;
 }
 
+int trstmi_normalize_columns(int field, int64_t d, int64_t N, double* frame, int64_t* zero_col) {
+  if ((field != TRSTMI_COMPLEX && field != TRSTMI_REAL) || d < 1 || N < 1 || !frame || !zero_col)
+    return TRSTMI_ERR_INVALID_ARG;
+  DevBuf df;
+  const int rc = frame_on_device(field, d, N, frame, 1, df, zero_col);
+  if (rc) return rc;
+  const size_t bytes = (size_t)(field == TRSTMI_COMPLEX ? 2 : 1) * d * N * sizeof(double);
+  return cudaMemcpy(frame, df.p, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? TRSTMI_OK : TRSTMI_ERR_CUDA;
+}
+
 int trstmi_cluster_sorted(const double* sorted, int64_t n, double cluster_tol, double* means, int64_t* count) {
   if (!(cluster_tol > 0.0) || !count || (n > 0 && (!sorted || !means))) return TRSTMI_ERR_INVALID_ARG;
   int64_t c = 0, k = 0;

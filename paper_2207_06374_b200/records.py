@@ -429,3 +429,58 @@ def make_run_record(method, result: SolveResult, method_config, started, finishe
         "timestamps": {"started": started, "finished": finished},
         "wall_time_seconds": result.wall_time_seconds,
     }
+
+
+# ------------------------------------------------------------------ targets (analysis.hpp:181-216)
+def conjecture1_target(d, N):
+    """analysis.hpp:181-187: 1/sqrt(d+1) for N in [d^2-d+2, d^2]."""
+    if d < 2:
+        return None
+    return 1.0 / math.sqrt(d + 1) if d * d - d + 2 <= N <= d * d else None
+
+
+def is_prime_power(n):
+    """analysis.hpp:189-204."""
+    if n < 2:
+        return False
+    p = 0
+    f = 2
+    while f * f <= n:
+        if n % f == 0:
+            p = f
+            break
+        f += 1
+    if p == 0:
+        return True
+    while n % p == 0:
+        n //= p
+    return n == 1
+
+
+def mub_removal_target(d, N):
+    """analysis.hpp:206-216: 1/sqrt(d) for prime-power d and N in [d^2+1, d^2+d]."""
+    if d < 2 or not is_prime_power(d):
+        return None
+    return 1.0 / math.sqrt(d) if d * d + 1 <= N <= d * (d + 1) else None
+
+
+def column_norms(frame, d, N, field=abi.COMPLEX):
+    f = _complex_view(frame, d, N, field).reshape(N, 2 * d)
+    return np.sqrt((f * f).sum(axis=1))
+
+
+def is_normalized(frame, d, N, field=abi.COMPLEX, tol=1e-12):
+    """frame.hpp:51-56."""
+    return bool(np.all(np.abs(column_norms(frame, d, N, field) - 1.0) <= tol))
+
+
+def normalize_columns(frame, d, N, field=abi.COMPLEX):
+    """frame.hpp:60-69 on the GPU (raises ZeroColumnError like the reference)."""
+    f = np.ascontiguousarray(frame, np.float64).reshape(-1).copy()
+    zc = ctypes.c_int64(-1)
+    rc = load_library().trstmi_normalize_columns(field, d, N, _p(f), ctypes.byref(zc))
+    if rc == abi.TRSTMI_ERR_ZERO_COLUMN:
+        raise ZeroColumnError(zc.value)
+    if rc:
+        raise RuntimeError("trstmi_normalize_columns failed (%d)" % rc)
+    return f
