@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
     }
     __syncthreads();
     const int imax = min(GIC, d - i0);
-    for (int ii = 0; ii < imax; ++ii) {
+    auto step = [&](int ii) {
       double ar[4], ai[4], br[4], bi[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
@@ -168,6 +168,12 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
             re[a][b] = fma(ar[a], br[b], re[a][b]);
           }
         }
+    };
+    if (imax == GIC) {  // full stage: compile-time trip count
+#pragma unroll 4
+      for (int ii = 0; ii < GIC; ++ii) step(ii);
+    } else {
+      for (int ii = 0; ii < imax; ++ii) step(ii);
     }
   }
   double best = MODE == 0 ? 0.0 : 0.0;
@@ -373,6 +379,9 @@ __global__ void __launch_bounds__(256) large_coef(LargeEval E) {
 // the next k-step's loads overlap this step's FMAs.  The rb == 0 CTAs also
 // sum the c*u tile into the t chunk partials (ascending k, add).
 constexpr int GM = 64, GK = 16, GRB = 64;  // columns, k-step, rows per CTA
+#ifndef GG_UNROLL
+#define GG_UNROLL 4
+#endif
 constexpr int GG_BUF = GK * GM * 3 + GK * GRB * 2;  // doubles per pipeline buffer
 constexpr size_t GG_SMEM = 2 * GG_BUF * sizeof(double);
 
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) tc[c] = __dadd_rn(tc[c], sCU[kk * GM + tm + 16 * c]);
     }
-    for (int kk = 0; kk < kmax; ++kk) {
+    auto step = [&](int kk) {
       double pr[4], pi[4], fr[RT], fi[RT];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -472,6 +481,12 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
             ar[r][c] = fma(fr[r], pr[c], ar[r][c]);
           }
         }
+    };
+    if (kmax == GK) {  // full step: a compile-time trip count lets loads run ahead of the FMAs
+#pragma unroll 4
+      for (int kk = 0; kk < GK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kmax; ++kk) step(kk);
     }
     __syncthreads();  // buffer b is refilled by the issue two steps on
   }
