@@ -23,7 +23,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxe
                  "-Xcompiler", "-fPIC,-ffp-contract=off,-O2", "-I", os.path.join(HERE, "..", "include")]
 
 # (complex, S, stored-Gram layout): the set kernel_table.hpp declares
-INSTANCES = [(c, s, g) for c in (1, 0) for (s, g) in ((32, 1), (128, 1), (128, 0), (256, 1), (256, 0), (512, 1))]
+INSTANCES = [(c, s, g) for c in (1, 0) for (s, g) in ((64, 1), (128, 1), (128, 0), (256, 1), (256, 0), (512, 1))]
 
 
 def _run(cmd):

@@ -13,13 +13,13 @@ struct KernelSet {
 };
 
 #define TRSTMI_DECL(f, s, l) const KernelSet* trstmi_kernels_##f##_##s##_##l(int d);
-TRSTMI_DECL(c, 32, g)
+TRSTMI_DECL(c, 64, g)
 TRSTMI_DECL(c, 128, g)
 TRSTMI_DECL(c, 128, r)
 TRSTMI_DECL(c, 256, g)
 TRSTMI_DECL(c, 256, r)
 TRSTMI_DECL(c, 512, g)
-TRSTMI_DECL(r, 32, g)
+TRSTMI_DECL(r, 64, g)
 TRSTMI_DECL(r, 128, g)
 TRSTMI_DECL(r, 128, r)
 TRSTMI_DECL(r, 256, g)
@@ -29,12 +29,12 @@ TRSTMI_DECL(r, 512, g)
 
 inline const KernelSet* find_kernels(bool cplx, int d, int S, int gs) {
   if (cplx) {
-    if (S == 32 && gs) return trstmi_kernels_c_32_g(d);
+    if (S == 64 && gs) return trstmi_kernels_c_64_g(d);
     if (S == 128) return gs ? trstmi_kernels_c_128_g(d) : trstmi_kernels_c_128_r(d);
     if (S == 256) return gs ? trstmi_kernels_c_256_g(d) : trstmi_kernels_c_256_r(d);
     if (S == 512 && gs) return trstmi_kernels_c_512_g(d);
   } else {
-    if (S == 32 && gs) return trstmi_kernels_r_32_g(d);
+    if (S == 64 && gs) return trstmi_kernels_r_64_g(d);
     if (S == 128) return gs ? trstmi_kernels_r_128_g(d) : trstmi_kernels_r_128_r(d);
     if (S == 256) return gs ? trstmi_kernels_r_256_g(d) : trstmi_kernels_r_256_r(d);
     if (S == 512 && gs) return trstmi_kernels_r_512_g(d);

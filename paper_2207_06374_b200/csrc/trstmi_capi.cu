@@ -86,11 +86,13 @@ struct trstmi_ctx {
 // Small-frame kernel choice for a shape: CTA width S (= the CAS reduction
 // width) and pair layout.  Candidates in order; the first whose anneal
 // shared memory fits one SM (227 KB) wins, none -> the large-frame path.
-//   dim <= 64      S = 32   stored Gram (padded / unpadded)
+//   dim <= 64      S = 64   stored Gram (padded / unpadded)
 //   dim <= 256     S = 128  stored Gram, else Gram recomputed
 //   larger         S = 512  stored Gram when even S = 256 leaves one CTA per
-//                           SM (16 warps instead of 8), else S = 256 stored
-//                           Gram, else recomputed
+//                           SM (16 warps instead of 8); S = 128 stored Gram
+//                           when there are <= 2048 pairs (4 trials per SM hide
+//                           the fixed per-evaluation costs); else S = 256
+//                           stored Gram, else recomputed
 struct SmallMode {
   bool ok;
   int S, gs, pad;
@@ -117,8 +119,8 @@ static SmallMode small_mode(int field, long long d, long long N) {
     ++nc;
   };
   if (dim <= 64) {
-    add(32, 1, 1);
-    add(32, 1, 0);
+    add(64, 1, 1);  // tiny frames: per-trial latency binds (config 1 runs 64 trials on 148 SMs)
+    add(64, 1, 0);
   } else if (dim <= 256) {
     add(128, 1, 1);
     add(128, 1, 0);
@@ -127,6 +129,10 @@ static SmallMode small_mode(int field, long long d, long long N) {
     if (gs_ok && small_bytes(field, d, N, 256, 1, 1) > kMax / 2) {
       add(512, 1, 1);
       add(512, 1, 0);
+    }
+    if (N * (N - 1) / 2 <= 2048) {  // few pairs: fixed per-evaluation costs bind -> 4 trials per SM
+      add(128, 1, 1);
+      add(128, 1, 0);
     }
     add(256, 1, 1);
     add(256, 1, 0);

@@ -28,7 +28,7 @@ def bits(a):
 
 def test_path_rule():
     from paper_2207_06374_b200 import api
-    assert api.lanes(C, 2, 100) == 512 and api.lanes(C, 6, 36) == 256 and api.lanes(R, 4, 10) == 32
+    assert api.lanes(C, 2, 100) == 512 and api.lanes(C, 6, 36) == 128 and api.lanes(R, 4, 10) == 64
     assert api.lanes(C, 2, 150) == 256  # too big for the stored-Gram layout: Gram recomputed
     for field, d, N in LARGE + [(R, 64, 1024), (C, 128, 4096)]:
         assert api.lanes(field, d, N) == 32768

@@ -259,7 +259,8 @@ def test_nonfinite_start_fails_like_the_reference(ctx):
 # (trstmi_small_layout: 0 Gram recomputed, 1 stored Gram, 2 stored Gram in
 # bank-padded rows): the same bits whichever layout runs
 LAYOUTS = [(C, 1, 128, 0, 128), (C, 1, 140, 0, 256), (C, 1, 116, 1, 128), (C, 2, 110, 1, 256),
-           (C, 3, 100, 1, 512), (C, 2, 80, 2, 512), (C, 3, 44, 2, 256), (C, 1, 35, 2, 128),
+           (C, 3, 100, 1, 512), (C, 2, 80, 2, 512), (C, 3, 44, 2, 128), (C, 2, 65, 2, 256), (C, 1, 35, 2, 128),
+           (R, 4, 10, 2, 64),
            (R, 2, 150, 0, 256), (R, 4, 40, 2, 128)]
 
 
