@@ -229,7 +229,21 @@ static cudaError_t launch_grad_gemm(const LargeEval& L, int cols, int d, int K, 
 template <bool CPLX>
 static void launch_coef(const LargeEval& L, cudaStream_t st) {
   const int nt = (L.N + GT - 1) / GT;
-  large_coef<CPLX><<<nt * (nt + 1) / 2, 256, 0, st>>>(L);
+  large_coef<CPLX><<<dim3(nt * (nt + 1) / 2, GT / 16), 256, 0, st>>>(L);
+}
+
+// K3a + K3b: the weights over the owned rows with a full grid, then the z chains
+static int launch_weights(const LargeEval& L, int nzb, cudaStream_t st) {  // returns the launch count
+  const long long p0 = (long long)L.m0 * L.N - (long long)L.m0 * (L.m0 + 1) / 2;
+  const long long p1 = (long long)L.m1 * L.N - (long long)L.m1 * (L.m1 + 1) / 2;
+  const long long n = p1 - p0;
+  if (n < (1LL << 21)) {  // small frames (config 4): one fused kernel, a launch fewer per evaluation
+    large_weights<true><<<nzb, ZLANES, 0, st>>>(L);
+    return 1;
+  }
+  large_exp<<<(unsigned)std::min<long long>((n + 511) / 512, 148LL * 16), 256, 0, st>>>(L);
+  large_weights<false><<<nzb, ZLANES, 0, st>>>(L);
+  return 2;
 }
 
 static LargeEval make_eval(Engine* E, const Shape& sh, const double* x, const double* dir, double sc, double delta,
@@ -255,14 +269,14 @@ int eval(Engine* E, const Shape& sh, const double* x, const double* dir, double 
   if (sh.cplx) large_gram<true, 0><<<tiles, 256, 0, st>>>(L, nullptr, nullptr);
   else large_gram<false, 0><<<tiles, 256, 0, st>>>(L, nullptr, nullptr);
   const int nzb = (sh.N + ZROWS - 1) / ZROWS;
-  large_weights<<<nzb, ZLANES, 0, st>>>(L);
+  const int wl = launch_weights(L, nzb, st);
   large_zreduce<<<1, 32, 0, st>>>(L, nzb);
   if (sh.cplx) launch_coef<true>(L, st);
   else launch_coef<false>(L, st);
   if (sh.cplx) LCHK(launch_grad_gemm<true>(L, sh.N, sh.d, sh.K, st));
   else LCHK(launch_grad_gemm<false>(L, sh.N, sh.d, sh.K, st));
   large_finalize<<<(sh.dim + 255) / 256, 256, 0, st>>>(L);
-  g_large_launches += 8;
+  g_large_launches += 7 + wl;
   LCHK(cudaGetLastError());
   LCHK(cudaMemcpyAsync(E->h_scal, w.scal, 3 * 8, cudaMemcpyDeviceToHost, st));
   LCHK(cudaMemcpyAsync(E->h_scal + 4, w.zero_col, 4, cudaMemcpyDeviceToHost, st));
@@ -352,7 +366,8 @@ static int eval_sharded(Engine* E, const Shape& sh, const double* x, const doubl
     NCHK(ncclAllReduce(E->w.smax, E->w.smax, 1, ncclUint64, ncclMax, E->nccl, st));
   }
   // phase B: weights of the shard's pairs, z partials of its 16-row blocks
-  for (int r : ranks) large_weights<<<nzb, ZLANES, 0, st>>>(Ls[r]);
+  int wl = 0;
+  for (int r : ranks) wl += launch_weights(Ls[r], nzb, st);
   LCHK(cudaGetLastError());
   // exchange: every rank's z-block partials to every rank
   auto zslice = [&](int r, int* b0, int* cnt) {
@@ -392,7 +407,7 @@ static int eval_sharded(Engine* E, const Shape& sh, const double* x, const doubl
     }
   }
   LCHK(cudaGetLastError());
-  g_large_launches += (long long)ranks.size() * 8;
+  g_large_launches += (long long)ranks.size() * 7 + wl;
   if (!E->virtual_ranks) {  // gradient column slices to every rank
     NCHK(ncclGroupStart());
     for (int r = 0; r < G; ++r) {

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(NORM_THREADS) large_normalize(LargeEval E) {
   const int j0 = blockIdx.x * NC;
   const int nc = min(NC, E.N - j0);
   const long long base = (long long)j0 * L;
-  for (int e = threadIdx.x; e < nc * L; e += NORM_THREADS) {
+#pragma unroll 8
+  for (int e = threadIdx.x; e < nc * L; e += NORM_THREADS) {  // unrolled: several loads in flight
     const int c = e / L, q = e - c * L;
     const double xv = E.x[base + e];
     ncol[c * LP + q] = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[base + e]));
@@ -234,10 +235,39 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
   }
 }
 
-// ---- K3: weights; z partial of each block of ZROWS rows (one CTA per block,
-// 256 CAS lanes over the block's contiguous pair range)
+// ---- K3b: z partial of each block of ZROWS rows (one CTA per block, 256
+// CAS lanes over the block's contiguous pair range); rows before a shard's
+// first row: the weights of its owned columns
 constexpr int ZROWS = 16;
 constexpr int ZLANES = 256;
+// ---- K3a: w = exp((x - s)/delta) in place over the pairs of the owned rows
+// [m0, m1) (a contiguous pair range), all threads of the grid; Markstein
+// quotients and the branch-free exp core (== IEEE division + cas_exp).
+__global__ void __launch_bounds__(256) large_exp(LargeEval E) {
+  const double s = __longlong_as_double((long long)*E.smax_bits);
+  const double cut = __dmul_rn(kUnderflowCut, E.delta);
+  const double yd = __drcp_rn(E.delta);
+  const bool chk = !(s >= 0x1.0p-800);  // else every nonzero |x - s| >= 2^-854 (Markstein exact)
+  const long long N = E.N, m0 = E.m0, m1 = E.m1;
+  const long long p0 = m0 * N - m0 * (m0 + 1) / 2, p1 = m1 * N - m1 * (m1 + 1) / 2;
+  double* __restrict__ X = E.X;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long p = p0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < p1; p += 2 * stride) {
+    const long long q = p + stride;
+    const bool v2 = q < p1;
+    const double d1 = __dsub_rn(X[p], s), d2 = v2 ? __dsub_rn(X[q], s) : 0.0;
+    double y1 = div_fast(d1, E.delta, yd), y2 = div_fast(d2, E.delta, yd);
+    if (chk) {
+      if (d1 < 0.0 && d1 > -0x1.0p-900) y1 = __ddiv_rn(d1, E.delta);
+      if (d2 < 0.0 && d2 > -0x1.0p-900) y2 = __ddiv_rn(d2, E.delta);
+    }
+    const double e1 = cas_exp_core(y1), e2 = cas_exp_core(y2);  // the core domain wherever !(diff < cut)
+    X[p] = (d1 < cut) ? 0.0 : e1;
+    if (v2) X[q] = (d2 < cut) ? 0.0 : e2;
+  }
+}
+
+template <bool FUSED>
 __global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
   __shared__ double wt[ZLANES / 32];
   const double s = __longlong_as_double((long long)*E.smax_bits);
@@ -257,30 +287,41 @@ __global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
     return;
   }
   const long long p0 = r0 * N - r0 * (r0 + 1) / 2, p1 = r1 * N - r1 * (r1 + 1) / 2;
-  const double yd = __drcp_rn(E.delta);
-  const bool chk = !(s >= 0x1.0p-800);  // else every nonzero |x - s| >= 2^-854 (Markstein exact)
   double* __restrict__ X = E.X;
   double zp = 0.0;
-  // four independent pairs per step (lane order l, l+256, l+512, l+768 is
-  // also the CAS z order), all loads issued before the stores
-  for (long long p = p0 + threadIdx.x; p < p1; p += 4 * ZLANES) {
-    double xv[4], w[4];
+  if (FUSED) {  // weights computed here (small frames: one launch fewer per evaluation)
+    const double yd = __drcp_rn(E.delta);
+    const bool chk = !(s >= 0x1.0p-800);  // else every nonzero |x - s| >= 2^-854 (Markstein exact)
+    for (long long p = p0 + threadIdx.x; p < p1; p += 4 * ZLANES) {
+      double xv[4], w[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = (p + u * ZLANES < p1) ? X[p + u * ZLANES] : 0.0;
+      for (int u = 0; u < 4; ++u) xv[u] = (p + u * ZLANES < p1) ? X[p + u * ZLANES] : 0.0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double diff = __dsub_rn(xv[u], s);
-      double y = div_fast(diff, E.delta, yd);
-      if (chk && diff < 0.0 && diff > -0x1.0p-900) y = __ddiv_rn(diff, E.delta);
-      const double e = cas_exp_core(y);  // the core domain wherever !(diff < cut)
-      w[u] = (diff < cut) ? 0.0 : e;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (p + u * ZLANES < p1) {
-        X[p + u * ZLANES] = w[u];
-        zp = __dadd_rn(zp, w[u]);
+      for (int u = 0; u < 4; ++u) {
+        const double diff = __dsub_rn(xv[u], s);
+        double y = div_fast(diff, E.delta, yd);
+        if (chk && diff < 0.0 && diff > -0x1.0p-900) y = __ddiv_rn(diff, E.delta);
+        const double e = cas_exp_core(y);  // the core domain wherever !(diff < cut)
+        w[u] = (diff < cut) ? 0.0 : e;
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (p + u * ZLANES < p1) {
+          X[p + u * ZLANES] = w[u];
+          zp = __dadd_rn(zp, w[u]);
+        }
+      }
+    }
+  } else {
+    // w written by large_exp; lane l sums its pairs l, l+256, ... in order (the
+    // CAS z order), four loads in flight
+    for (long long p = p0 + threadIdx.x; p < p1; p += 4 * ZLANES) {
+      double w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = (p + u * ZLANES < p1) ? X[p + u * ZLANES] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (p + u * ZLANES < p1) zp = __dadd_rn(zp, w[u]);
     }
   }
 #pragma unroll
@@ -321,8 +362,8 @@ __global__ void __launch_bounds__(256) large_coef(LargeEval E) {
   if (jb * GT >= E.m1) return;  // rows >= m1 are not owned
   const double z = E.scal[1];
   const double yz = __drcp_rn(z);
-  for (int h = 0; h < GT; h += HR) {
-    __syncthreads();
+  {  // pass h = rows [h, h + HR) of the tile (gridDim.y = GT / HR passes)
+    const int h = blockIdx.y * HR;
 #pragma unroll
     for (int i = 0; i < HR * GT / 256; ++i) {
       const int e = threadIdx.x + 256 * i;
