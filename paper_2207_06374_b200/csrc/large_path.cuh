@@ -64,7 +64,7 @@ struct LargeEval {
 // with coalesced loads, then thread c runs column c's CAS norm chain
 // (ascending fma) and divides by Markstein quotients (== IEEE division).
 constexpr int NORM_THREADS = 128;
-__host__ __device__ inline int norm_cols(int L) { return max(1, min(128, 6144 / (L + 1))); }
+__host__ __device__ inline int norm_cols(int L) { return max(1, min(32, 2048 / (L + 1))); }
 __host__ __device__ inline size_t norm_smem(int L) { return (size_t)norm_cols(L) * (L + 1) * sizeof(double); }
 __global__ void __launch_bounds__(NORM_THREADS) large_normalize(LargeEval E) {
   extern __shared__ double ncol[];  // NC x (L + 1)
@@ -73,11 +73,26 @@ __global__ void __launch_bounds__(NORM_THREADS) large_normalize(LargeEval E) {
   const int j0 = blockIdx.x * NC;
   const int nc = min(NC, E.N - j0);
   const long long base = (long long)j0 * L;
-#pragma unroll 8
-  for (int e = threadIdx.x; e < nc * L; e += NORM_THREADS) {  // unrolled: several loads in flight
-    const int c = e / L, q = e - c * L;
-    const double xv = E.x[base + e];
-    ncol[c * LP + q] = (E.sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(E.sc, E.dir[base + e]));
+  for (int e0 = 0; e0 < nc * L; e0 += 8 * NORM_THREADS) {  // eight loads in flight per thread
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * NORM_THREADS + threadIdx.x;
+      double xv = 0.0;
+      if (e < nc * L) {
+        xv = E.x[base + e];
+        if (E.sc != 0.0) xv = __dadd_rn(xv, __dmul_rn(E.sc, E.dir[base + e]));
+      }
+      v[u] = xv;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * NORM_THREADS + threadIdx.x;
+      if (e < nc * L) {
+        const int c = e / L, q = e - c * L;
+        ncol[c * LP + q] = v[u];
+      }
+    }
   }
   __syncthreads();
   for (int c = threadIdx.x; c < nc; c += NORM_THREADS) {
@@ -339,10 +354,16 @@ __global__ void __launch_bounds__(ZLANES) large_weights(LargeEval E) {
 
 // ---- K4: z = block sums added in row order; F = s + delta log z
 __global__ void large_zreduce(LargeEval E, int nblocks) {
+  __shared__ double zs[1024];
+  const bool staged = nblocks <= 1024;
+  if (staged)
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) zs[b] = E.zpart[b];  // loads in parallel
+  __syncthreads();
   if (threadIdx.x != 0) return;
   E.scal[0] = __longlong_as_double((long long)*E.smax_bits);
-  double z = E.zpart[0];
-  for (int b = 1; b < nblocks; ++b) z = __dadd_rn(z, E.zpart[b]);
+  const double* zp = staged ? zs : E.zpart;
+  double z = zp[0];
+  for (int b = 1; b < nblocks; ++b) z = __dadd_rn(z, zp[b]);
   E.scal[1] = z;
   E.scal[2] = __dadd_rn(E.scal[0], __dmul_rn(E.delta, cas_log(z)));
 }
