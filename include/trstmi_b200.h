@@ -255,6 +255,13 @@ int trstmi_normalize_columns(int field, int64_t d, int64_t N, double* frame, int
 /* cluster_magnitudes (frame.hpp:96-118) over an ascending array: means of the
  * single-linkage clusters (gap > cluster_tol), sequential sums; *count means. */
 int trstmi_cluster_sorted(const double* sorted, int64_t n, double cluster_tol, double* means, int64_t* count);
+/* distortion_mc (beamforming.hpp:78-163): Monte-Carlo quantisation
+ * distortion E[1 - max_i |<phi_i, h>|^2 / |h|^2] of a complex d x N codebook
+ * (interleaved, unit columns) over samples channels h ~ CN(0, I), blocks of
+ * 4096 samples each with SplitMix64(mix_seed(seed, block)).  GPU Box-Muller
+ * (CUDA log/sin/cos): within an ulp of the reference's draws. */
+int trstmi_distortion_mc(int64_t d, int64_t N, const double* codebook, uint64_t samples, uint64_t seed,
+                         double* estimate, double* std_error);
 /* check_tight's deviation (analysis.hpp:76-84): max |(Phi Phi*)(r,s) - (N/d) I| */
 int trstmi_frame_operator_deviation(int field, int64_t d, int64_t N, const double* frame, double* deviation);
 

@@ -226,6 +226,55 @@ std::int64_t orc_hvp(int field, std::int64_t d, std::int64_t N, int lanes, const
   return -1;
 }
 
+// distortion_mc (beamforming.hpp:78-163) restated with the CAS orders (the
+// checker of trstmi_distortion_mc): blocks of 4096 samples, SplitMix64 per
+// block, overlaps |conj(phi_i) . h|^2 by ascending fma chains, moments summed
+// sequentially per block and then in block order.
+int orc_distortion_mc(std::int64_t d, std::int64_t N, const double* book, std::uint64_t samples,
+                      std::uint64_t seed, double* estimate, double* std_error) {
+  if (samples < 1 || N < 1) return 1;
+  const std::uint64_t B = 4096, nblocks = (samples + B - 1) / B;
+  double sum = 0.0, sum_sq = 0.0;
+  std::vector<double> h(2 * d);
+  for (std::uint64_t b = 0; b < nblocks; ++b) {
+    Rng rng(mix_seed(seed, b));
+    const std::uint64_t count = std::min(B, samples - b * B);
+    double bs = 0.0, bq = 0.0;
+    for (std::uint64_t s = 0; s < count; ++s) {
+      double norm_sq = 0.0;
+      do {
+        for (std::int64_t i = 0; i < d; ++i) rng.complex_normal(&h[2 * i], &h[2 * i + 1]);
+        norm_sq = 0.0;
+        for (std::int64_t q = 0; q < 2 * d; ++q) norm_sq = std::fma(h[q], h[q], norm_sq);
+      } while (norm_sq < kZeroColumnTol * kZeroColumnTol);
+      double best = 0.0;
+      for (std::int64_t i = 0; i < N; ++i) {
+        const double* col = book + i * 2 * d;
+        double re = 0.0, im = 0.0;
+        for (std::int64_t q = 0; q < d; ++q) {
+          const double ar = col[2 * q], ai = col[2 * q + 1], hr = h[2 * q], hi = h[2 * q + 1];
+          re = std::fma(ar, hr, re);
+          re = std::fma(ai, hi, re);
+          im = std::fma(ar, hi, im);
+          im = std::fma(-ai, hr, im);
+        }
+        const double ov = re * re + im * im;
+        if (ov > best) best = ov;
+      }
+      const double dsq = std::max(0.0, 1.0 - best / norm_sq);
+      bs += dsq;
+      bq += dsq * dsq;
+    }
+    sum += bs;
+    sum_sq += bq;
+  }
+  const double n = static_cast<double>(samples);
+  *estimate = sum / n;
+  *std_error = 0.0;
+  if (samples > 1) *std_error = std::sqrt(std::max(0.0, (sum_sq - n * *estimate * *estimate) / (n - 1.0)) / n);
+  return 0;
+}
+
 // offdiagonal_magnitudes (frame.hpp:80-91) of a frame, CAS |G| (the checker
 // of trstmi_offdiag_magnitudes)
 void orc_offdiag_magnitudes(int field, std::int64_t d, std::int64_t N, const double* frame, double* mags) {

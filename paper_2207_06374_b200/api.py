@@ -68,6 +68,7 @@ def load_library():
     lib.trstmi_cluster_sorted.argtypes = [vp, c_i64, c_dbl, vp, vp]
     lib.trstmi_frame_operator_deviation.argtypes = [c_int, c_i64, c_i64, vp, vp]
     lib.trstmi_normalize_columns.argtypes = [c_int, c_i64, c_i64, vp, vp]
+    lib.trstmi_distortion_mc.argtypes = [c_i64, c_i64, vp, ctypes.c_uint64, ctypes.c_uint64, vp, vp]
     lib.trstmi_welch_bound.argtypes = [c_i64, c_i64]
     lib.trstmi_welch_bound.restype = c_dbl
     lib.trstmi_default_schedule.argtypes = [c_i64, c_dbl, vp, c_int]

@@ -6,11 +6,11 @@ the reference's tools/main.cpp (/root/reference/proj/tools/main.cpp):
   sweep    --d --N-range a:b --out DIR [...]              cmd_sweep   main.cpp:198-267
   bounds   --d (--N | --N-range a:b) [--out CSV]          cmd_bounds  main.cpp:123-152
   certify  --in FRAME(.json|.csv) [--tol 1e-4]            cmd_certify main.cpp:161-196
+  distortion --in FRAME [--samples N] [--seed S]          cmd_distortion main.cpp:269-279
 
 Same output lines, CSV columns and JSON keys as the reference.  --threads is
 accepted for compatibility (restarts run as a GPU batch).  The altproj method
-and the distortion command are outside this build's scope (SURVEY.md §8f
-rank 4) and exit with status 2.
+is outside this build's scope and exits with status 2.
 
   python -m paper_2207_06374_b200.cli solve --d 2 --N 4 --restarts 20 --seed 7 --out r.json
 """
@@ -139,6 +139,20 @@ def cmd_certify(args):
     return 0
 
 
+def cmd_distortion(args):
+    """main.cpp:269-279: Monte-Carlo quantisation distortion of a codebook (GPU)."""
+    if args.samples < 1:
+        print("error: --samples must be positive", file=sys.stderr)
+        return 2
+    f, d, N = load_normalized(args.inp)
+    est = rec.distortion_mc(f, d, N, args.samples, args.seed)
+    mags = rec.offdiagonal_magnitudes(f, d, N)
+    mu = float(mags.max()) if mags.size and mags.max() > 0.0 else 0.0
+    print(json.dumps({"estimate": est["estimate"], "std_error": est["std_error"], "samples": est["samples"],
+                      "coherence_of_codebook": mu}, indent=2))
+    return 0
+
+
 def cmd_sweep(args):
     lo, hi = parse_range(args.N_range)
     if lo < args.d:
@@ -206,12 +220,19 @@ def main(argv=None):
     p.add_argument("--N", type=int, default=0)
     p.add_argument("--N-range", dest="N_range", default="")
     p.add_argument("--out", default="")
+    p = sub.add_parser("distortion", help="Monte-Carlo quantization distortion of a codebook")
+    p.add_argument("--in", dest="inp", required=True)
+    p.add_argument("--samples", type=int, default=1000000)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--sigma", type=float, default=1.0, help="noise variance (accepted, as the reference)")
+    p.add_argument("--Es", type=float, default=1.0, help="mean symbol energy (accepted, as the reference)")
     p = sub.add_parser("certify", help="bounds, tightness and certificates of a frame file")
     p.add_argument("--in", dest="inp", required=True)
     p.add_argument("--tol", type=float, default=rec.kDefaultCertificateTol)
     args = ap.parse_args(argv)
     try:
-        return {"solve": cmd_solve, "sweep": cmd_sweep, "bounds": cmd_bounds, "certify": cmd_certify}[args.cmd](args)
+        return {"solve": cmd_solve, "sweep": cmd_sweep, "bounds": cmd_bounds, "certify": cmd_certify,
+                "distortion": cmd_distortion}[args.cmd](args)
     except (ValueError, rec.FileFormatError) as e:  # usage / file errors exit 2 like the reference
         print("error: %s" % e, file=sys.stderr)
         return 2

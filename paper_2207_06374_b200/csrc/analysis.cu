@@ -8,6 +8,10 @@
 //                              (sequential, host: the reference's sum order)
 //   trstmi_frame_operator_deviation  check_tight     analysis.hpp:76-84
 //                              (max |Phi Phi* - (N/d) I| entry)
+//   trstmi_distortion_mc       distortion_mc           beamforming.hpp:78-163
+//                              (Monte-Carlo quantisation distortion of a codebook:
+//                              one warp per 4096-sample block, the block's own
+//                              SplitMix64 stream, codeword overlaps across lanes)
 //
 // |z| = sqrt(re*re + im*im) throughout (the CAS coherence, DESIGN.md §3 item
 // 10; the reference's std::abs is hypot — at most an ulp apart, far inside
@@ -22,7 +26,9 @@
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <cmath>
 #include <string>
+#include <vector>
 
 #include "../../include/trstmi_b200.h"
 #include "small_path.cuh"
@@ -106,6 +112,103 @@ __global__ void an_frame_operator(const double* __restrict__ f, int cplx, int d,
   if ((threadIdx.x & 31) == 0) atomicMax(dev_bits, (unsigned long long)__double_as_longlong(m));
 }
 
+// SplitMix64 (rng.hpp:13-64) on the device: the integer stream is exact; the
+// Box-Muller normals use CUDA's log/sqrt/sin/cos, within an ulp or two of glibc.
+struct DevRng {
+  unsigned long long state;
+  bool has_spare;
+  double spare;
+  __device__ unsigned long long next_u64() {
+    unsigned long long z = (state += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  __device__ double uniform() { return (double)(next_u64() >> 11) * 0x1.0p-53; }
+  __device__ double normal() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    double u1 = uniform();
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    const double u2 = uniform();
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    const double theta = __dmul_rn(2.0 * 3.14159265358979323846, u2);
+    spare = __dmul_rn(r, sin(theta));
+    has_spare = true;
+    return __dmul_rn(r, cos(theta));
+  }
+};
+
+__device__ __forceinline__ unsigned long long dev_mix_seed(unsigned long long seed, unsigned long long index) {
+  unsigned long long z = seed + (index + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+constexpr unsigned long long kDistortionBlock = 4096;  // beamforming.hpp:61
+
+// one warp per block b: lane 0 draws h (d complex normals, rejection as the
+// reference), every lane scores codewords lane, lane+32, ... (|<phi_i, h>|^2,
+// ascending-index fma chain), warp max, lane 0 accumulates the block moments
+// sequentially (sum, sum of squares) like distortion_block.
+__global__ void an_distortion(const double* __restrict__ book, int d, int N, unsigned long long samples,
+                              unsigned long long seed, double* __restrict__ moments) {
+  extern __shared__ double hs[];  // 2d per warp
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned long long b = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const unsigned long long nblocks = (samples + kDistortionBlock - 1) / kDistortionBlock;
+  if (b >= nblocks) return;
+  double* h = hs + (size_t)wib * 2 * d;
+  const unsigned long long start = b * kDistortionBlock;
+  const unsigned long long count = min(kDistortionBlock, samples - start);
+  DevRng rng{dev_mix_seed(seed, b), false, 0.0};
+  double sum = 0.0, sum_sq = 0.0;
+  for (unsigned long long s = 0; s < count; ++s) {
+    double norm_sq = 0.0;
+    if (lane == 0) {
+      do {
+        for (int i = 0; i < d; ++i) {
+          const double a = rng.normal(), c = rng.normal();
+          h[2 * i] = __dmul_rn(a, 0.70710678118654752440);
+          h[2 * i + 1] = __dmul_rn(c, 0.70710678118654752440);
+        }
+        norm_sq = 0.0;
+        for (int q = 0; q < 2 * d; ++q) norm_sq = fma(h[q], h[q], norm_sq);
+      } while (norm_sq < kZeroColumnTol * kZeroColumnTol);
+    }
+    __syncwarp();
+    double best = 0.0;
+    for (int i = lane; i < N; i += 32) {
+      const double* col = book + (long long)i * 2 * d;
+      double re = 0.0, im = 0.0;
+      for (int q = 0; q < d; ++q) {  // conj(phi_i) . h
+        const double ar = col[2 * q], ai = col[2 * q + 1], hr = h[2 * q], hi = h[2 * q + 1];
+        re = fma(ar, hr, re);
+        re = fma(ai, hi, re);
+        im = fma(ar, hi, im);
+        im = fma(-ai, hr, im);
+      }
+      const double ov = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+      best = ov > best ? ov : best;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, off));
+    if (lane == 0) {
+      const double dsq = fmax(0.0, __dsub_rn(1.0, __ddiv_rn(best, norm_sq)));
+      sum = __dadd_rn(sum, dsq);
+      sum_sq = __dadd_rn(sum_sq, __dmul_rn(dsq, dsq));
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    moments[2 * b] = sum;
+    moments[2 * b + 1] = sum_sq;
+  }
+}
+
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() {
@@ -174,6 +277,41 @@ int trstmi_normalize_columns(int field, int64_t d, int64_t N, double* frame, int
   if (rc) return rc;
   const size_t bytes = (size_t)(field == TRSTMI_COMPLEX ? 2 : 1) * d * N * sizeof(double);
   return cudaMemcpy(frame, df.p, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? TRSTMI_OK : TRSTMI_ERR_CUDA;
+}
+
+int trstmi_distortion_mc(int64_t d, int64_t N, const double* codebook, uint64_t samples, uint64_t seed,
+                         double* estimate, double* std_error) {
+  if (d < 1 || N < 1 || !codebook || !estimate || !std_error) return TRSTMI_ERR_INVALID_ARG;
+  if (samples < 1) return TRSTMI_ERR_INVALID_ARG;  // distortion_mc: samples >= 1
+  const unsigned long long nblocks = (samples + kDistortionBlock - 1) / kDistortionBlock;
+  DevBuf db, dm;
+  const size_t bytes = (size_t)2 * d * N * sizeof(double);
+  if (cudaMalloc(&db.p, bytes) != cudaSuccess || cudaMalloc(&dm.p, (size_t)2 * nblocks * sizeof(double)) != cudaSuccess)
+    return TRSTMI_ERR_CUDA;
+  if (cudaMemcpy(db.p, codebook, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return TRSTMI_ERR_CUDA;
+  constexpr int WPB = 4;  // warps (sample blocks) per CTA
+  const size_t smem = (size_t)WPB * 2 * d * sizeof(double);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(an_distortion, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return TRSTMI_ERR_UNSUPPORTED;
+  an_distortion<<<(unsigned)((nblocks + WPB - 1) / WPB), 32 * WPB, smem>>>((const double*)db.p, (int)d, (int)N,
+                                                                          samples, seed, (double*)dm.p);
+  std::vector<double> m((size_t)2 * nblocks);
+  if (cudaMemcpy(m.data(), dm.p, m.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return TRSTMI_ERR_CUDA;
+  double sum = 0.0, sum_sq = 0.0;  // block moments in block order (beamforming.hpp:142-147)
+  for (unsigned long long b = 0; b < nblocks; ++b) {
+    sum += m[2 * b];
+    sum_sq += m[2 * b + 1];
+  }
+  const double n = static_cast<double>(samples);
+  *estimate = sum / n;
+  *std_error = 0.0;
+  if (samples > 1) {
+    const double var = std::max(0.0, (sum_sq - n * *estimate * *estimate) / (n - 1.0));
+    *std_error = std::sqrt(var / n);
+  }
+  return TRSTMI_OK;
 }
 
 int trstmi_cluster_sorted(const double* sorted, int64_t n, double cluster_tol, double* means, int64_t* count) {

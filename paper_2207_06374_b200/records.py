@@ -484,3 +484,18 @@ def normalize_columns(frame, d, N, field=abi.COMPLEX):
     if rc:
         raise RuntimeError("trstmi_normalize_columns failed (%d)" % rc)
     return f
+
+
+def distortion_mc(codebook, d, N, samples, seed, field=abi.COMPLEX):
+    """beamforming.hpp:78-163 on the GPU: {"estimate", "std_error", "samples"}."""
+    if samples < 1:
+        raise ValueError("distortion_mc: samples >= 1")
+    if N < 1:
+        raise ValueError("distortion_mc: empty codebook")
+    f = np.ascontiguousarray(_complex_view(codebook, d, N, field))
+    est, se = ctypes.c_double(), ctypes.c_double()
+    rc = load_library().trstmi_distortion_mc(d, N, _p(f), ctypes.c_uint64(samples), ctypes.c_uint64(seed),
+                                             ctypes.byref(est), ctypes.byref(se))
+    if rc:
+        raise RuntimeError("trstmi_distortion_mc failed (%d)" % rc)
+    return {"estimate": est.value, "std_error": se.value, "samples": int(samples)}

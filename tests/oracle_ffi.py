@@ -55,6 +55,7 @@ def lib():
         L.orc_coherence.argtypes = [c_int, i64, i64, vp, c_int, vp, vp]
         L.orc_coherence.restype = i64
         L.orc_offdiag_magnitudes.argtypes = [c_int, i64, i64, vp, vp]
+        L.orc_distortion_mc.argtypes = [i64, i64, vp, u64, u64, vp, vp]
         L.orc_solve_batch.argtypes = [vp, c_int, i64, vp, vp, vp, vp, vp, vp, c_int]
         L.orc_time_solve_batch.argtypes = [vp, c_int, i64, vp, vp, c_int, vp, vp]
         L.orc_time_solve_batch.restype = dbl
@@ -184,3 +185,10 @@ def offdiag_magnitudes(field, d, N, frame):
 
 def mix_seed(seed, index):
     return int(lib().orc_mix_seed(seed, index))
+
+
+def distortion_mc(d, N, book, samples, seed):
+    book = np.ascontiguousarray(book, np.float64)
+    est, se = ctypes.c_double(), ctypes.c_double()
+    assert lib().orc_distortion_mc(d, N, _p(book), samples, seed, ctypes.byref(est), ctypes.byref(se)) == 0
+    return est.value, se.value

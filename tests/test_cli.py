@@ -43,6 +43,7 @@ def test_usage_errors_exit_with_code_2():  # test_cli.cpp:81-89
     assert run_cli("bounds", "--d", "2", "--N-range", "9:3")[0] == 2
     assert run_cli("certify", "--in", "/no/such/file.json")[0] == 2
     assert run_cli("distortion", "--in", "/no/such/file.json")[0] == 2
+    assert run_cli("distortion", "--in", "/no/such/file.json", "--samples", "0")[0] == 2
     assert run_cli("nonsense")[0] == 2
 
 
@@ -81,3 +82,18 @@ def test_sweep_writes_records_and_monotone_csv():  # main.cpp:198-267
         assert mono == sorted(mono)
         for n in (3, 4, 5):
             assert json.load(open(os.path.join(tmp, "run_d2_N%d.json" % n)))["schema_version"] == 1
+
+
+@pytest.mark.gpu
+def test_distortion_is_deterministic_for_a_fixed_seed():  # test_cli.cpp:107-123
+    from tests.test_records import sic_2_4
+    from paper_2207_06374_b200 import records as rec
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "sic.json")
+        rec.save_frame(path, sic_2_4(), 2, 4)
+        a = run_cli("distortion", "--in", path, "--samples", "20000", "--seed", "5")
+        b = run_cli("distortion", "--in", path, "--samples", "20000", "--seed", "5")
+        assert a[0] == 0 and a == b
+        report = json.loads(a[1])
+        assert report["samples"] == 20000 and 0.0 <= report["estimate"] <= 1.0
+        assert abs(report["coherence_of_codebook"] - 1.0 / math.sqrt(3.0)) <= 1e-12

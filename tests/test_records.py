@@ -230,3 +230,54 @@ def test_identical_solves_give_identical_records_modulo_timing():  # test_io.cpp
         return j
 
     assert without_timing() == without_timing()
+
+
+# ------------------------------------------------------------------ GPU: MISO codebook distortion
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,N,samples,seed", [(2, 4, 50000, 99), (3, 9, 20000, 7), (2, 1, 9000, 5), (4, 40, 5000, 3)])
+def test_distortion_matches_the_oracle(d, N, samples, seed):
+    book = sic_2_4() if (d, N) == (2, 4) else (sic_3_9() if (d, N) == (3, 9) else
+                                                  orc.random_frames(C, d, N, 11, 0, 1)[0][0])
+    if (d, N) == (2, 1):
+        book = np.array([1.0, 0.0, 0.0, 0.0])
+    g = rec.distortion_mc(book, d, N, samples, seed)
+    eo, so = orc.distortion_mc(d, N, book, samples, seed)
+    # the integer SplitMix64 streams are identical; CUDA and glibc log/sin/cos
+    # differ by an ulp or two, so the estimates agree to rounding
+    assert abs(g["estimate"] - eo) <= 1e-12 * max(1.0, abs(eo))
+    assert abs(g["std_error"] - so) <= 1e-9 * max(so, 1e-300)
+
+
+@pytest.mark.gpu
+def test_distortion_of_a_single_codeword_in_d2_is_one_half():  # test_beamforming.cpp:107-126
+    est = rec.distortion_mc(np.array([1.0, 0.0, 0.0, 0.0]), 2, 1, 200000, 5)
+    assert abs(est["estimate"] - 0.5) <= 4.0 * est["std_error"]
+
+
+@pytest.mark.gpu
+def test_distortion_estimates_are_deterministic():  # test_beamforming.cpp:128-137
+    a = rec.distortion_mc(sic_2_4(), 2, 4, 50000, 99)
+    b = rec.distortion_mc(sic_2_4(), 2, 4, 50000, 99)
+    assert a == b
+
+
+@pytest.mark.gpu
+def test_standard_error_scales_like_inverse_sqrt_samples():  # test_beamforming.cpp:139-147
+    small = rec.distortion_mc(sic_2_4(), 2, 4, 40000, 3)
+    large = rec.distortion_mc(sic_2_4(), 2, 4, 160000, 3)
+    assert 0.0 <= small["estimate"] <= 1.0
+    assert abs(small["std_error"] / large["std_error"] - 2.0) <= 0.6
+
+
+@pytest.mark.gpu
+def test_codebook_orderings():  # test_beamforming.cpp:149-180
+    big = orc.random_frames(C, 2, 12, 246, 0, 1)[0][0]
+    small = big[:5 * 4]
+    ds, db = rec.distortion_mc(small, 2, 5, 100000, 31), rec.distortion_mc(big, 2, 12, 100000, 31)
+    assert db["estimate"] <= ds["estimate"] + 2.0 * (ds["std_error"] + db["std_error"])
+    basis, sic = rec.distortion_mc(identity_frame(2), 2, 2, 200000, 13), rec.distortion_mc(sic_2_4(), 2, 4, 200000, 13)
+    assert sic["estimate"] + 3.0 * (sic["std_error"] + basis["std_error"]) < basis["estimate"]
+    dense = orc.random_frames(C, 2, 1000, 135, 0, 1)[0][0]
+    sparse = orc.random_frames(C, 2, 10, 135, 0, 1)[0][0]
+    dd, dsp = rec.distortion_mc(dense, 2, 1000, 20000, 77), rec.distortion_mc(sparse, 2, 10, 20000, 77)
+    assert dd["estimate"] < dsp["estimate"] and dd["estimate"] < 0.01
