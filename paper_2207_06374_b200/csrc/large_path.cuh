@@ -444,7 +444,8 @@ constexpr int GM = 64, GK = 16, GRB = 64;  // columns, k-step, rows per CTA
 #ifndef GG_UNROLL
 #define GG_UNROLL 4
 #endif
-constexpr int GG_BUF = GK * GM * 3 + GK * GRB * 2;  // doubles per pipeline buffer
+constexpr int GFS = GRB + 1;  // phi tile row stride: the k-major cp.async writes hit distinct banks
+constexpr int GG_BUF = GK * GM * 3 + GK * GFS * 2;  // doubles per pipeline buffer
 constexpr size_t GG_SMEM = 2 * GG_BUF * sizeof(double);
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
@@ -480,10 +481,10 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
       const int kk = e % GK, r = e / GK;
       const int k = k0 + kk, row = rb * GRB + r;
       const bool v = k < k_hi && row < d;
-      double* dst = base + 3 * GK * GM + kk * GRB + r;
+      double* dst = base + 3 * GK * GM + kk * GFS + r;
       if (CPLX) {
         cp_async8(dst, E.phiT + (v ? (long long)(2 * row) * N + k : 0), v);
-        cp_async8(dst + GK * GRB, E.phiT + (v ? (long long)(2 * row + 1) * N + k : 0), v);
+        cp_async8(dst + GK * GFS, E.phiT + (v ? (long long)(2 * row + 1) * N + k : 0), v);
       } else {
         cp_async8(dst, E.phiT + (v ? (long long)row * N + k : 0), v);
       }
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
     const double* sPi = sPr + GK * GM;
     const double* sCU = sPr + 2 * GK * GM;
     const double* sFr = sPr + 3 * GK * GM;
-    const double* sFi = sFr + GK * GRB;
+    const double* sFi = sFr + GK * GFS;
     const int kmax = min(GK, k_hi - k0);
     if (tsum) {
       for (int kk = 0; kk < kmax; ++kk)
@@ -527,8 +528,8 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
       }
 #pragma unroll
       for (int r = 0; r < RT; ++r) {
-        fr[r] = sFr[kk * GRB + tr + 16 * r];
-        if (CPLX) fi[r] = sFi[kk * GRB + tr + 16 * r];
+        fr[r] = sFr[kk * GFS + tr + 16 * r];
+        if (CPLX) fi[r] = sFi[kk * GFS + tr + 16 * r];
       }
 #pragma unroll
       for (int r = 0; r < RT; ++r)
