@@ -121,12 +121,21 @@ __device__ __forceinline__ void tile_of(int t, int nt, int& jb, int& kb) {  // u
   kb = row + rem;
 }
 
+// cp.async (global -> shared, 8 bytes, zero-fill when !valid) for the
+// double-buffered operand streams of the Gram and gradient GEMMs
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
+
 // ---- K2: tile (jb <= kb) of GT x GT pairs, 256 threads x (4 j x 4 k).
 // mode 0: objective (store x, G, max); mode 1: coherence (per-tile max |G| and first argmax).
 template <bool CPLX, int MODE>
 __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, long long* tile_arg) {
-  __shared__ double sa[2][GIC][GT];
-  __shared__ double sb[2][GIC][GT];
+  __shared__ double gbuf[2][4][GIC][GT];  // [buffer][re a, re b, im a, im b][i][column], cp.async-filled
   __shared__ double red_v[8];
   __shared__ long long red_i[8];
   const int N = E.N, d = E.d;
@@ -144,19 +153,31 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) re[a][b] = im[a][b] = 0.0;
-  for (int i0 = 0; i0 < d; i0 += GIC) {
-    __syncthreads();
+  auto issue = [&](int i0, int bsel) {
     for (int e = tid; e < GIC * GT; e += 256) {
       const int ii = e / GT, c = e - ii * GT;
       const int i = i0 + ii;
       const int j = jb * GT + c, k = kb * GT + c;
-      const bool iv = i < d;
-      sa[0][ii][c] = (iv && j < N) ? E.phiT[(long long)(CPLX ? 2 * i : i) * N + j] : 0.0;
-      sb[0][ii][c] = (iv && k < N) ? E.phiT[(long long)(CPLX ? 2 * i : i) * N + k] : 0.0;
+      const bool iv = i < d, vj = iv && j < N, vk = iv && k < N;
+      const long long rr = (long long)(CPLX ? 2 * i : i) * N;
+      cp_async8(&gbuf[bsel][0][ii][c], E.phiT + (vj ? rr + j : 0), vj);
+      cp_async8(&gbuf[bsel][1][ii][c], E.phiT + (vk ? rr + k : 0), vk);
       if (CPLX) {
-        sa[1][ii][c] = (iv && j < N) ? E.phiT[(long long)(2 * i + 1) * N + j] : 0.0;
-        sb[1][ii][c] = (iv && k < N) ? E.phiT[(long long)(2 * i + 1) * N + k] : 0.0;
+        cp_async8(&gbuf[bsel][2][ii][c], E.phiT + (vj ? rr + N + j : 0), vj);
+        cp_async8(&gbuf[bsel][3][ii][c], E.phiT + (vk ? rr + N + k : 0), vk);
       }
+    }
+    cp_async_commit();
+  };
+  const int nst = (d + GIC - 1) / GIC;
+  if (nst > 0) issue(0, 0);
+  for (int stg = 0; stg < nst; ++stg) {
+    const int i0 = stg * GIC, bsel = stg & 1;
+    if (stg + 1 < nst) {
+      issue(i0 + GIC, bsel ^ 1);  // the next stage streams in while this one computes
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
     const int imax = min(GIC, d - i0);
@@ -164,11 +185,11 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
       double ar[4], ai[4], br[4], bi[4];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        ar[a] = sa[0][ii][tj + 16 * a];
-        br[a] = sb[0][ii][tk + 16 * a];
+        ar[a] = gbuf[bsel][0][ii][tj + 16 * a];
+        br[a] = gbuf[bsel][1][ii][tk + 16 * a];
         if (CPLX) {
-          ai[a] = sa[1][ii][tj + 16 * a];
-          bi[a] = sb[1][ii][tk + 16 * a];
+          ai[a] = gbuf[bsel][2][ii][tj + 16 * a];
+          bi[a] = gbuf[bsel][3][ii][tk + 16 * a];
         }
       }
 #pragma unroll
@@ -191,6 +212,7 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
     } else {
       for (int ii = 0; ii < imax; ++ii) step(ii);
     }
+    __syncthreads();  // this buffer is refilled by the issue of the next stage but one
   }
   double best = MODE == 0 ? 0.0 : 0.0;
   long long barg = LLONG_MAX;
@@ -448,13 +470,6 @@ constexpr int GFS = GRB + 1;  // phi tile row stride: the k-major cp.async write
 constexpr int GG_BUF = GK * GM * 3 + GK * GFS * 2;  // doubles per pipeline buffer
 constexpr size_t GG_SMEM = 2 * GG_BUF * sizeof(double);
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int NPEND>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory"); }
 
 template <bool CPLX>
 __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
