@@ -211,18 +211,25 @@ static cudaError_t launch_normalize(const LargeEval& L, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// K6 with its two cp.async pipeline buffers (GG_SMEM bytes, > 48 KB opt-in)
-template <bool CPLX>
-static cudaError_t launch_grad_gemm(const LargeEval& L, int cols, int d, int K, cudaStream_t st) {
+// K6 with its two cp.async pipeline buffers (gg_smem(GMT) bytes, > 48 KB opt-in);
+// 32-column CTAs for small frames (twice the CTAs of a single-wave grid)
+template <bool CPLX, int GMT>
+static cudaError_t launch_grad_gemm_t(const LargeEval& L, int cols, int d, int K, cudaStream_t st) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(large_grad_gemm<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GG_SMEM);
+    attr = cudaFuncSetAttribute(large_grad_gemm<CPLX, GMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)gg_smem(GMT));
   });
   if (attr != cudaSuccess) return attr;
-  dim3 gg((cols + GM - 1) / GM, (d + GRB - 1) / GRB, K);
-  large_grad_gemm<CPLX><<<gg, 256, GG_SMEM, st>>>(L);
+  dim3 gg((cols + GMT - 1) / GMT, (d + GRB - 1) / GRB, K);
+  large_grad_gemm<CPLX, GMT><<<gg, 256, gg_smem(GMT), st>>>(L);
   return cudaGetLastError();
+}
+template <bool CPLX>
+static cudaError_t launch_grad_gemm(const LargeEval& L, int cols, int d, int K, cudaStream_t st) {
+  if (L.N <= 2048) return launch_grad_gemm_t<CPLX, 32>(L, cols, d, K, st);
+  return launch_grad_gemm_t<CPLX, 64>(L, cols, d, K, st);
 }
 
 // K5 over the upper-triangular pair tiles

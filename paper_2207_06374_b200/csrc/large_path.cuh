@@ -467,36 +467,37 @@ constexpr int GM = 64, GK = 16, GRB = 64;  // columns, k-step, rows per CTA
 #define GG_UNROLL 4
 #endif
 constexpr int GFS = GRB + 1;  // phi tile row stride: the k-major cp.async writes hit distinct banks
-constexpr int GG_BUF = GK * GM * 3 + GK * GFS * 2;  // doubles per pipeline buffer
-constexpr size_t GG_SMEM = 2 * GG_BUF * sizeof(double);
+__host__ __device__ constexpr size_t gg_smem(int gmt) { return 2 * (size_t)(GK * gmt * 3 + GK * GFS * 2) * sizeof(double); }
 
 
-template <bool CPLX>
+template <bool CPLX, int GMT>
 __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
+  constexpr int CW = GMT / 16;                                      // columns per thread
+  constexpr int BUF = GK * GMT * 3 + GK * GFS * 2;                  // doubles per pipeline buffer
   constexpr int RT = 4;  // complex rows / real rows per thread
   extern __shared__ double gsm[];
   const int N = E.N, d = E.d, K = E.K;
-  const int mb = blockIdx.x + E.m0 / GM, rb = blockIdx.y, ch = blockIdx.z;
+  const int mb = blockIdx.x + E.m0 / GMT, rb = blockIdx.y, ch = blockIdx.z;
   const int k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
   const int tid = threadIdx.x;
   const int tm = tid & 15, tr = tid >> 4;
   const bool tsum = rb == 0 && tr == 0;  // threads 0..15: t of columns tm + 16c, ascending k (c*u add)
   auto issue = [&](int k0, int b) {
-    double* base = gsm + b * GG_BUF;
-    for (int e = tid; e < GK * GM; e += 256) {
-      const int kk = e / GM, c = e - kk * GM;
-      const int k = k0 + kk, m = mb * GM + c;
+    double* base = gsm + b * BUF;
+    for (int e = tid; e < GK * GMT; e += 256) {
+      const int kk = e / GMT, c = e - kk * GMT;
+      const int k = k0 + kk, m = mb * GMT + c;
       const bool v = k < k_hi && m < E.m1;
       const long long o = v ? (long long)k * N + m : 0;
       cp_async8(base + e, E.PR + o, v);
-      if (CPLX) cp_async8(base + GK * GM + e, E.PI + o, v);
-      if (rb == 0) cp_async8(base + 2 * GK * GM + e, E.CU + o, v);
+      if (CPLX) cp_async8(base + GK * GMT + e, E.PI + o, v);
+      if (rb == 0) cp_async8(base + 2 * GK * GMT + e, E.CU + o, v);
     }
     for (int e = tid; e < GK * GRB; e += 256) {  // lanes along k: 128-byte runs of phi rows
       const int kk = e % GK, r = e / GK;
       const int k = k0 + kk, row = rb * GRB + r;
       const bool v = k < k_hi && row < d;
-      double* dst = base + 3 * GK * GM + kk * GFS + r;
+      double* dst = base + 3 * GK * GMT + kk * GFS + r;
       if (CPLX) {
         cp_async8(dst, E.phiT + (v ? (long long)(2 * row) * N + k : 0), v);
         cp_async8(dst + GK * GFS, E.phiT + (v ? (long long)(2 * row + 1) * N + k : 0), v);
@@ -506,12 +507,14 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
     }
     cp_async_commit();
   };
-  double ar[RT][4], ai[RT][4];
+  double ar[RT][CW], ai[RT][CW];
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) ar[r][c] = ai[r][c] = 0.0;
-  double tc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c = 0; c < CW; ++c) ar[r][c] = ai[r][c] = 0.0;
+  double tc[CW];
+#pragma unroll
+  for (int c = 0; c < CW; ++c) tc[c] = 0.0;
   const int nsteps = (k_hi - k_lo + GK - 1) / GK;
   if (nsteps > 0) issue(k_lo, 0);
   for (int st = 0; st < nsteps; ++st) {
@@ -523,23 +526,23 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* sPr = gsm + b * GG_BUF;
-    const double* sPi = sPr + GK * GM;
-    const double* sCU = sPr + 2 * GK * GM;
-    const double* sFr = sPr + 3 * GK * GM;
+    const double* sPr = gsm + b * BUF;
+    const double* sPi = sPr + GK * GMT;
+    const double* sCU = sPr + 2 * GK * GMT;
+    const double* sFr = sPr + 3 * GK * GMT;
     const double* sFi = sFr + GK * GFS;
     const int kmax = min(GK, k_hi - k0);
     if (tsum) {
       for (int kk = 0; kk < kmax; ++kk)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tc[c] = __dadd_rn(tc[c], sCU[kk * GM + tm + 16 * c]);
+        for (int c = 0; c < CW; ++c) tc[c] = __dadd_rn(tc[c], sCU[kk * GMT + tm + 16 * c]);
     }
     auto step = [&](int kk) {
-      double pr[4], pi[4], fr[RT], fi[RT];
+      double pr[CW], pi[CW], fr[RT], fi[RT];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        pr[c] = sPr[kk * GM + tm + 16 * c];
-        if (CPLX) pi[c] = sPi[kk * GM + tm + 16 * c];
+      for (int c = 0; c < CW; ++c) {
+        pr[c] = sPr[kk * GMT + tm + 16 * c];
+        if (CPLX) pi[c] = sPi[kk * GMT + tm + 16 * c];
       }
 #pragma unroll
       for (int r = 0; r < RT; ++r) {
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
 #pragma unroll
       for (int r = 0; r < RT; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < CW; ++c) {
           if (CPLX) {
             ar[r][c] = fma(fr[r], pr[c], ar[r][c]);
             ar[r][c] = fma(-fi[r], pi[c], ar[r][c]);
@@ -570,16 +573,16 @@ __global__ void __launch_bounds__(256) large_grad_gemm(LargeEval E) {
   }
   if (tsum) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int m = mb * GM + tm + 16 * c;
+    for (int c = 0; c < CW; ++c) {
+      const int m = mb * GMT + tm + 16 * c;
       if (m < E.m1) E.tpart[(long long)ch * N + m] = tc[c];
     }
   }
 #pragma unroll
   for (int r = 0; r < RT; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int row = rb * GRB + tr + 16 * r, m = mb * GM + tm + 16 * c;
+    for (int c = 0; c < CW; ++c) {
+      const int row = rb * GRB + tr + 16 * r, m = mb * GMT + tm + 16 * c;
       if (row < d && m < E.m1) {
         double* out = E.part + (long long)ch * E.dim + (long long)m * E.L;
         if (CPLX) {
