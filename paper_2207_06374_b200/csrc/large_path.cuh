@@ -33,6 +33,7 @@ constexpr int LS_THREADS = 256;
 constexpr int LS_LANES = LS_CTAS * LS_THREADS;  // 32768 CAS lanes
 constexpr int GT = 64;                           // Gram tile (pairs per side)
 constexpr int GIC = 8;                           // Gram i-rows staged per step
+constexpr int GNBUF = 3;                         // Gram stage buffers (two in flight)
 
 struct LargeEval {
   int cplx, d, N, L, dim, K, squared;
@@ -135,9 +136,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // mode 0: objective (store x, G, max); mode 1: coherence (per-tile max |G| and first argmax).
 template <bool CPLX, int MODE>
 __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, long long* tile_arg) {
-  __shared__ double gbuf[2][4][GIC][GT];  // [buffer][re a, re b, im a, im b][i][column], cp.async-filled
-  __shared__ double red_v[8];
-  __shared__ long long red_i[8];
+  // [buffer][re a, re b, (im a, im b)][i][column], cp.async-filled; three
+  // buffers so two stages stream in while one computes (48 KB complex).
+  __shared__ double gbuf[GNBUF][CPLX ? 4 : 2][GIC][GT];
+  double* red_v = &gbuf[0][0][0][0];  // reused after the last stage's barrier
+  long long* red_i = reinterpret_cast<long long*>(&gbuf[0][0][1][0]);
   const int N = E.N, d = E.d;
   const int nt = (N + GT - 1) / GT;
   int jb, kb;
@@ -154,32 +157,31 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
 #pragma unroll
     for (int b = 0; b < 4; ++b) re[a][b] = im[a][b] = 0.0;
   auto issue = [&](int i0, int bsel) {
-    for (int e = tid; e < GIC * GT; e += 256) {
-      const int ii = e / GT, c = e - ii * GT;
-      const int i = i0 + ii;
-      const int j = jb * GT + c, k = kb * GT + c;
-      const bool iv = i < d, vj = iv && j < N, vk = iv && k < N;
-      const long long rr = (long long)(CPLX ? 2 * i : i) * N;
-      cp_async8(&gbuf[bsel][0][ii][c], E.phiT + (vj ? rr + j : 0), vj);
-      cp_async8(&gbuf[bsel][1][ii][c], E.phiT + (vk ? rr + k : 0), vk);
-      if (CPLX) {
-        cp_async8(&gbuf[bsel][2][ii][c], E.phiT + (vj ? rr + N + j : 0), vj);
-        cp_async8(&gbuf[bsel][3][ii][c], E.phiT + (vk ? rr + N + k : 0), vk);
+    if (i0 < d) {
+      for (int e = tid; e < GIC * GT; e += 256) {
+        const int ii = e / GT, c = e - ii * GT;
+        const int i = i0 + ii;
+        const int j = jb * GT + c, k = kb * GT + c;
+        const bool iv = i < d, vj = iv && j < N, vk = iv && k < N;
+        const long long rr = (long long)(CPLX ? 2 * i : i) * N;
+        cp_async8(&gbuf[bsel][0][ii][c], E.phiT + (vj ? rr + j : 0), vj);
+        cp_async8(&gbuf[bsel][1][ii][c], E.phiT + (vk ? rr + k : 0), vk);
+        if (CPLX) {
+          cp_async8(&gbuf[bsel][CPLX ? 2 : 0][ii][c], E.phiT + (vj ? rr + N + j : 0), vj);
+          cp_async8(&gbuf[bsel][CPLX ? 3 : 1][ii][c], E.phiT + (vk ? rr + N + k : 0), vk);
+        }
       }
     }
-    cp_async_commit();
+    cp_async_commit();  // always one group per stage index (empty past d) so the wait counts stay uniform
   };
   const int nst = (d + GIC - 1) / GIC;
-  if (nst > 0) issue(0, 0);
+  issue(0, 0);
+  issue(GIC, 1);
   for (int stg = 0; stg < nst; ++stg) {
-    const int i0 = stg * GIC, bsel = stg & 1;
-    if (stg + 1 < nst) {
-      issue(i0 + GIC, bsel ^ 1);  // the next stage streams in while this one computes
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    const int i0 = stg * GIC, bsel = stg % GNBUF;
+    cp_async_wait<1>();  // stage stg landed (stage stg + 1 may still be in flight)
+    __syncthreads();     // ... for every thread, and every thread is done computing stage stg - 1
+    issue(i0 + 2 * GIC, (stg + 2) % GNBUF);  // refills the buffer of stage stg - 1
     const int imax = min(GIC, d - i0);
     auto step = [&](int ii) {
       double ar[4], ai[4], br[4], bi[4];
@@ -188,8 +190,8 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
         ar[a] = gbuf[bsel][0][ii][tj + 16 * a];
         br[a] = gbuf[bsel][1][ii][tk + 16 * a];
         if (CPLX) {
-          ai[a] = gbuf[bsel][2][ii][tj + 16 * a];
-          bi[a] = gbuf[bsel][3][ii][tk + 16 * a];
+          ai[a] = gbuf[bsel][CPLX ? 2 : 0][ii][tj + 16 * a];
+          bi[a] = gbuf[bsel][CPLX ? 3 : 1][ii][tk + 16 * a];
         }
       }
 #pragma unroll
@@ -212,8 +214,9 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
     } else {
       for (int ii = 0; ii < imax; ++ii) step(ii);
     }
-    __syncthreads();  // this buffer is refilled by the issue of the next stage but one
   }
+  cp_async_wait<0>();
+  __syncthreads();  // gbuf is reused by the reduction below
   double best = MODE == 0 ? 0.0 : 0.0;
   long long barg = LLONG_MAX;
 #pragma unroll
