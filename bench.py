@@ -6,24 +6,37 @@ Workload (BASELINE.json configs[1], the headline config that fits one GPU):
 complex lines in C^2, N = 100, 4096 independent seeded trials (trial i starts
 from random_frame(SplitMix64(mix_seed(0, i)))), each a full anneal() with
 TrustRegionConfig.max_outer = 500 (stage k capped at 500 + 50k, solver.hpp:187),
-default delta schedule at eps_target 1e-7.  One step = the whole batch.
+default delta schedule at eps_target 1e-7 (8 stages).
+
+A step is the full anneal of one slice of the config's trials (default 1024
+trials for config 2, so 4 consecutive steps cover the 4096 trials once; the
+driver's 20 steps cover them 5 times).  Warm-up steps anneal one SM-wave of
+trials (there is no JIT/autotune state to warm).  `e2e` repeats slice 0
+through the host-pointer C ABI (trstmi_solve_batch: H2D of start frames and
+generator states, D2H of parameters, frames and records inside the timed
+region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun: one rank per GPU, each rank anneals its own 4096
-trials (trial ids offset by rank; weak scaling), then an NCCL allgather of
-(best mu, trial id) and a broadcast of the winning frame (solver.hpp:256-267).
-Rank 0 prints one JSON line.
+N > 1 runs under torchrun, one rank per GPU.  Default --scaling strong: the
+config's trials are split into contiguous blocks (trstmi_shard_range, trial i
+on rank floor(i N / T)); each step anneals one slice of the rank's block; the
+best-of exchange is the product's NCCL path (trstmi_best_of_ranks: allgather
+of (mu, trial), broadcast of the winning frame).  --scaling weak gives every
+rank its own T trials.
 
---impl reference times the reference algorithm's CPU implementation on the
-host cores: the CAS oracle (oracle/, an Eigen-free restatement of the
-reference; the reference itself cannot be built here — DESIGN.md §5), all
-host threads, each step a bounded sample of the same workload.
+--impl reference times the reference's own CPU implementation on the host
+cores: the reference headers compiled unchanged against an Eigen-API shim
+(oracle/_ref), all host threads, each step one delta stage of a
+group of trials (one trial per thread); the value is taken over whole anneal
+cycles.  It loads nothing from the product library.
 """
 import argparse
 import ctypes
 import json
+import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -35,38 +48,61 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2207_06374_b200 import abi  # noqa: E402
+from paper_2207_06374_b200 import abi  # noqa: E402  (pure ctypes layouts; loads no native code)
 
 CONFIGS = {
-    # name: field, d, N, trials per GPU, max_outer, workload
+    # name: field, d, N, trials (config), max_outer, workload, default slice
     #   "anneal": the reference's full anneal (every delta stage)
     #   "stage0": the anneal's first stage (delta = 0.1) with that max_outer —
-    #             the fixed-work mode SURVEY.md §8d prescribes for configs 4-5,
-    #             whose full anneals (CG up to 2*dim per iteration) cannot be timed
-    "c1": (abi.REAL, 4, 10, 64, 200, "anneal"),
-    "c2": (abi.COMPLEX, 2, 100, 4096, 500, "anneal"),
-    "c3": (abi.COMPLEX, 6, 36, 1024, 1000, "anneal"),
-    "c4": (abi.REAL, 64, 1024, 256, 300, "stage0"),
-    "c5": (abi.COMPLEX, 128, 4096, 64, 100, "stage0"),
+    #             the fixed-work mode SURVEY.md §8d prescribes for configs 4-5
+    "c1": (abi.REAL, 4, 10, 64, 200, "anneal", 64),
+    "c2": (abi.COMPLEX, 2, 100, 4096, 500, "anneal", 1024),
+    "c3": (abi.COMPLEX, 6, 36, 1024, 1000, "anneal", 1024),
+    "c4": (abi.REAL, 64, 1024, 256, 300, "stage0", 256),
+    "c5": (abi.COMPLEX, 128, 4096, 64, 100, "stage0", 64),
     # config 5's single frame, Gram row-blocks sharded over the ranks (NCCL)
-    "c5frame": (abi.COMPLEX, 128, 4096, 1, 20, "stage0"),
+    "c5frame": (abi.COMPLEX, 128, 4096, 1, 20, "stage0", 1),
 }
+METRIC = "TR iterations/sec & Gram entries/sec (fp64, batched trials); % of roofline"
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 148 SMs x 64 DFMA/clk x 2 flop x 1965 MHz
+
+
+def default_schedule(N, eps=1e-7):
+    """default_delta_schedule (solver.hpp:64-82), restated so the reference
+    arm needs no native library for it."""
+    terminal = eps / (2.0 * math.log(N))
+    if terminal >= 1e-1:
+        return [10.0 * terminal, terminal]
+    out, delta = [], 1e-1
+    while delta > terminal * (1.0 + 1e-12):
+        out.append(delta)
+        delta /= 10.0
+    out.append(terminal)
+    return out
 
 
 def make_cfg(field, d, N, max_outer, workload):
     cfg = abi.default_cfg(field, d, N, max_outer)
     if workload == "stage0":
-        from paper_2207_06374_b200 import api
         cfg.n_stages = 1
-        cfg.schedule[0] = api.default_schedule(N)[0]
+        cfg.schedule[0] = default_schedule(N)[0]
     return cfg
-METRIC = "TR iterations/sec & Gram entries/sec (fp64, batched trials); % of roofline"
 
 
 def flops_per_eval(field, d, N):
     """the two dense contractions eval_objective performs
     (smoothing.hpp:104,147): 16 d N^2 (complex), 4 d N^2 (real)."""
     return (16 if field == abi.COMPLEX else 4) * d * N * N
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -114,70 +150,148 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(field, d, N, max_outer, trials, threads, first=0, workload="anneal"):
-    """Oracle (port of the reference algorithm) over `trials` anneals on
-    `threads` host threads; returns (seconds, outer iterations, evals)."""
+# ---------------------------------------------------------------------------- CPU (reference) runs
+def ref_cycle_sample(cfg, first, trials, threads, budget_s=None):
+    """The reference's own code (oracle/_ref) annealing trials [first,
+    first+trials) stage by stage on `threads` host threads.  Returns a list of
+    per-stage (seconds, outer iterations, evaluator calls) and the kind."""
+    from tests import ref_ffi
+    starts = None
+    if cfg.field == abi.REAL:  # real mode: start frames from the real random_frame (oracle restatement)
+        from tests import oracle_ffi
+        starts, _ = oracle_ffi.random_frames(cfg.field, cfg.d, cfg.N, 0, first, trials)
+    b = ref_ffi.Batch(cfg, 0, first, trials, starts)
+    out = []
+    t0 = time.perf_counter()
+    for k in range(b.ns):
+        sec, o, e, _ = b.run(k, k + 1, threads)
+        out.append((sec, o, e))
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    b.close()
+    return out, b.ns
+
+
+def port_cycle_sample(cfg, first, trials, threads):
+    """Fallback when oracle/_ref is absent (it is built where /root/reference
+    exists and shipped prebuilt): the CAS oracle port, full anneals."""
     from tests import oracle_ffi as orc
     L = orc.lib()
-    cfg = make_cfg(field, d, N, max_outer, workload)
-    S = abi.lanes_for(field, d, N)
-    params, st = orc.random_frames(field, d, N, 0, first, trials)
-    outer = ctypes.c_int64()
-    evals = ctypes.c_int64()
+    S = 32768 if cfg.d > 16 else 512
+    params, st = orc.random_frames(cfg.field, cfg.d, cfg.N, 0, first, trials)
+    outer, evals = ctypes.c_int64(), ctypes.c_int64()
     sec = L.orc_time_solve_batch(ctypes.byref(cfg), S, trials, ctypes.c_void_p(params.ctypes.data),
                                  ctypes.c_void_p(st.ctypes.data), threads, ctypes.byref(outer), ctypes.byref(evals))
-    return sec, outer.value, evals.value
+    return [(sec, outer.value, evals.value)]
+
+
+def ref_available():
+    from tests import ref_ffi
+    return ref_ffi.available()
+
+
+def cpu_cfg(args, field, d, N, max_outer, workload):
+    if workload == "stage0":  # CPU cost per eval at N >= 1024 is seconds: cap the stage
+        max_outer = min(max_outer, args.cpu_outer or (1 if N > 2048 else 2))
+    return make_cfg(field, d, N, max_outer, workload), max_outer
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU implementation of the reference algorithm."""
+    """--impl reference: the reference's CPU implementation on all host threads."""
     if rank != 0:
         return
-    field, d, N, trials, max_outer, workload = CONFIGS[args.config]
-    if workload == "stage0":
-        max_outer = min(max_outer, args.cpu_outer or (1 if N > 2048 else 3))
+    field, d, N, trials, max_outer, workload, _ = CONFIGS[args.config]
+    cfg, cpu_outer = cpu_cfg(args, field, d, N, max_outer, workload)
     threads = os.cpu_count() or 1
-    sample = args.cpu_trials or threads
+    group = args.cpu_trials or threads
     n = N * (N - 1) // 2
-    for _ in range(args.warmup):
-        cpu_sample(field, d, N, max_outer, min(sample, threads), threads, workload=workload)
-    secs, outs, evs = [], [], []
-    for _ in range(args.steps):
-        s, o, e = cpu_sample(field, d, N, max_outer, sample, threads, workload=workload)
-        secs.append(s)
-        outs.append(o)
-        evs.append(e)
-    tot_s = sum(secs)
-    v = sum(outs) / tot_s
+    use_ref = ref_available()
+    ns = cfg.n_stages or len(default_schedule(N, cfg.eps_target))
+    cycles = max(1, int(round(args.steps / ns))) if args.steps > 0 else 0
+    if use_ref:
+        if args.warmup > 0:  # nothing to warm on a CPU; one short stage keeps the W contract visible
+            wc = make_cfg(field, d, N, 1, workload)
+            ref_cycle_sample(wc, 10 ** 6, 1, 1, budget_s=0)
+        secs, outs, evs = [], [], []
+        for c in range(cycles):
+            res, _ = ref_cycle_sample(cfg, c * group, group, threads)
+            for s, o, e in res:
+                secs.append(s)
+                outs.append(o)
+                evs.append(e)
+        kind = "reference"
+        sample = ("%d anneal cycle(s) of %d trials each (trials 0..%d of the seed-0 batch), one delta stage per step "
+                  "(%d stage steps), %d host threads; the reference's own headers (proj/include/trstmi) compiled "
+                  "unchanged against an Eigen-API shim (oracle/_ref, -O3 -DNDEBUG -std=c++20, naive loops for "
+                  "Eigen's products); CPU %s" % (cycles, group, cycles * group - 1, len(secs), threads, cpu_model()))
+    else:
+        secs, outs, evs = [], [], []
+        for c in range(cycles):
+            for s, o, e in port_cycle_sample(cfg, c * group, group, threads):
+                secs.append(s)
+                outs.append(o)
+                evs.append(e)
+        kind = "port"
+        sample = ("%d x %d full anneals on %d threads; CAS oracle port (oracle/_ref missing); CPU %s"
+                  % (cycles, group, threads, cpu_model()))
+    tot = sum(secs) or float("nan")
+    v = sum(outs) / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TR iterations/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / max(len(secs), 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "gram_entries_per_s": sum(evs) * n / tot_s, "evals_per_s": sum(evs) / tot_s,
-        "config": {"workload": "%s: %s d=%d N=%d, %d trials x anneal(max_outer=%d); CPU sample %d trials/step"
-                   % (args.config, "complex" if field == abi.COMPLEX else "real", d, N, trials, max_outer, sample),
-                   "trials": trials, "max_outer": max_outer, "seed": 0},
-        "cpu_baseline": {"value": v, "unit": "TR iterations/s", "cores": min(sample, threads), "kind": "port",
-                         "sample": "%d full anneals (trials 0..%d of the seed-0 batch) per step on %d threads; "
-                                   "oracle/ CAS restatement (reference not buildable: no Eigen)"
-                                   % (sample, sample - 1, threads)},
+        "gram_entries_per_s": sum(evs) * n / tot, "evals_per_s": sum(evs) / tot,
+        "config": {"workload": "%s: %s d=%d N=%d, trials x %s(max_outer=%d)"
+                   % (args.config, "complex" if field == abi.COMPLEX else "real", d, N,
+                      "anneal" if workload == "anneal" else "anneal stage 0", cpu_outer),
+                   "trials": trials, "max_outer": cpu_outer, "seed": 0},
+        "cpu_baseline": {"value": v, "unit": "TR iterations/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "TR iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline(args, field, d, N, workload):
+    """cpu_baseline of the GPU line: one whole anneal cycle of one trial per
+    host thread through the reference's code (oracle/_ref)."""
+    threads = os.cpu_count() or 1
+    group = args.cpu_trials or threads
+    n = N * (N - 1) // 2
+    cfg, cpu_outer = cpu_cfg(args, field, d, N, CONFIGS[args.config][4], workload)
+    if ref_available():
+        res, ns = ref_cycle_sample(cfg, 0, group, threads, budget_s=args.cpu_budget)
+        kind = "reference"
+        what = ("%d of %d delta stages of trials 0..%d (one trial per thread), the reference's own headers "
+                "compiled against an Eigen-API shim (oracle/_ref, -O3 -DNDEBUG, no -march)"
+                % (len(res), ns, group - 1))
+    else:
+        res = port_cycle_sample(cfg, 0, group, threads)
+        kind = "port"
+        what = "%d full anneals, CAS oracle port" % group
+    s = sum(r[0] for r in res)
+    o = sum(r[1] for r in res)
+    e = sum(r[2] for r in res)
+    return {"value": o / s, "unit": "TR iterations/s", "cores": threads, "kind": kind,
+            "sample": "%s; %.1f s on %d threads; CPU %s" % (what, s, threads, cpu_model()),
+            "gram_entries_per_s": e * n / s, "max_outer": cpu_outer}
+
+
+# ---------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--trials", type=int, default=0, help="override trials per rank (testing only)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--trials", type=int, default=0, help="override the config's trial count (testing only)")
+    ap.add_argument("--slice", type=int, default=0, help="trials per step per rank (default: the config's)")
     ap.add_argument("--cpu-trials", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds cap of the cpu_baseline cycle")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-outer", type=int, default=0,
-                    help="stage0 configs: outer iterations per CPU sample trial (default 3; 1 when N > 2048)")
+                    help="stage0 configs: outer iterations per CPU sample trial (default 2; 1 when N > 2048)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -195,69 +309,84 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    field, d, N, trials, max_outer, workload = CONFIGS[args.config]
+    field, d, N, T, max_outer, workload, slice_default = CONFIGS[args.config]
     if args.trials:
-        trials = args.trials
+        T = args.trials
     dim = abi.dim_of(field, d, N)
     n = N * (N - 1) // 2
     fpe = flops_per_eval(field, d, N)
     lib = api.load_library()
-    lib.trstmi_launch_count.restype = ctypes.c_longlong
-    lib.trstmi_measure_dfma_peak.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
     ctx = api.Context(local_rank)
     cfg = make_cfg(field, d, N, max_outer, workload)
     ns = cfg.n_stages or api.default_schedule_len(N)
-    first = rank * trials
-    sharded = args.config == "c5frame"
-    if sharded and world > 1:  # one frame, Gram row-blocks over the ranks
+    sharded_frame = args.config == "c5frame"
+
+    def nccl_id():
         obj = [api.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        ctx.set_shard(world, rank, obj[0])
-        first = 0
+        return ctypes.create_string_buffer(bytes(obj[0]), 128)
 
-    # inputs: start frames + generator states (host, pinned for e2e)
-    starts, rng0 = api.random_frames(field, d, N, 0, first, trials)
+    if world > 1:
+        ctx.check(lib.trstmi_comm_init(ctx.h, world, rank, nccl_id()), "comm_init")
+    if sharded_frame:  # one frame, Gram row-blocks over the ranks
+        if world > 1:
+            ctx.check(lib.trstmi_set_shard(ctx.h, world, rank, nccl_id()), "set_shard")
+        first, count = 0, T
+    elif args.scaling == "strong":  # the config's trials in contiguous blocks
+        f, c = ctypes.c_int64(), ctypes.c_int64()
+        ctx.check(lib.trstmi_shard_range(T, world, rank, ctypes.byref(f), ctypes.byref(c)), "shard_range")
+        first, count = f.value, c.value
+    else:
+        first, count = rank * T, T
+    slc = max(1, min(args.slice or slice_default, count))
+    n_slices = (count + slc - 1) // slc
+
+    # inputs: start frames + generator states of the rank's block (host), resident on the device
+    starts, rng0 = api.random_frames(field, d, N, 0, first, count)
     stream = torch.cuda.current_stream()
     sptr = ctypes.c_void_p(stream.cuda_stream)
     d_start = torch.from_numpy(starts).cuda()
-    d_params = torch.empty_like(d_start)
-    d_frames = torch.empty_like(d_start)
-    d_tout = torch.empty(trials * ctypes.sizeof(abi.TrialOut), dtype=torch.uint8, device="cuda")
-    d_sout = torch.empty(trials * ns * ctypes.sizeof(abi.StageOut), dtype=torch.uint8, device="cuda")
+    d_params = torch.empty((slc, dim), dtype=torch.float64, device="cuda")
+    d_frames = torch.empty_like(d_params)
+    d_best = torch.zeros(dim, dtype=torch.float64, device="cuda")
+    d_tout = torch.empty(slc * ctypes.sizeof(abi.TrialOut), dtype=torch.uint8, device="cuda")
+    d_sout = torch.zeros(slc * ns * ctypes.sizeof(abi.StageOut), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
-    h_tout = (abi.TrialOut * trials)()
+    h_tout = (abi.TrialOut * slc)()
+    best = {"mu": float("nan"), "trial": -1}
 
-    def device_step():
-        rng = rng0.copy()
-        d_params.copy_(d_start)
+    def device_step(lo, cnt):
+        rng = rng0[lo:lo + cnt].copy()
+        d_params[:cnt].copy_(d_start[lo:lo + cnt])
         flush.fill_(1)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rc = lib.trstmi_solve_batch_dev(ctx.h, ctypes.byref(cfg), trials, ctypes.c_void_p(d_params.data_ptr()),
+        rc = lib.trstmi_solve_batch_dev(ctx.h, ctypes.byref(cfg), cnt, ctypes.c_void_p(d_params.data_ptr()),
                                         ctypes.c_void_p(rng.ctypes.data), ctypes.c_void_p(d_frames.data_ptr()),
                                         ctypes.c_void_p(d_tout.data_ptr()), ctypes.c_void_p(d_sout.data_ptr()),
                                         None, sptr)
         e1.record(stream)
         ctx.check(rc, "solve_batch_dev")
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / 1e3
-
-    def reduce_best():
-        """min over trials then over ranks, lowest trial id on ties (solver.hpp:256-263)."""
-        host = d_tout.cpu().numpy()  # keep the host copy alive across the memmove
-        ctypes.memmove(h_tout, host.ctypes.data, ctypes.sizeof(h_tout))
-        best, bi = None, -1
-        for t in range(trials):
+        host = d_tout[:cnt * ctypes.sizeof(abi.TrialOut)].cpu().numpy()
+        ctypes.memmove(h_tout, host.ctypes.data, host.nbytes)
+        outer = evals = 0
+        for t in range(cnt):  # best-of over the block (solver.hpp:256-263): strict <, ascending trial id
             r = h_tout[t]
-            if r.status == abi.TRIAL_OK and (best is None or r.coherence < best):
-                best, bi = r.coherence, t
-        outer = sum(h_tout[t].outer_iterations for t in range(trials))
-        evals = sum(h_tout[t].evals for t in range(trials))
-        return best, bi, outer, evals
+            outer += r.outer_iterations
+            evals += r.evals
+            gid = first + lo + t
+            if r.status == abi.TRIAL_OK and (best["trial"] < 0 or r.coherence < best["mu"] or
+                                             (r.coherence == best["mu"] and gid < best["trial"])):
+                best["mu"], best["trial"] = r.coherence, gid
+                d_best.copy_(d_frames[t])
+        return e0.elapsed_time(e1) / 1e3, outer, evals
 
+    # warm-up: one SM wave of trials through the same entry point
     for _ in range(max(args.warmup, 0)):
-        device_step()
+        device_step(0, min(slc, 148))
+    best.update(mu=float("nan"), trial=-1)
     launches0 = lib.trstmi_launch_count()
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -265,21 +394,22 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     times, outers, evals_l = [], [], []
-    best_mu, best_trial = None, -1
-    for _ in range(args.steps):
-        times.append(device_step())
-        best_mu, best_trial, o, e = reduce_best()
+    for i in range(args.steps):
+        s = i % n_slices
+        lo = s * slc
+        t, o, e = device_step(lo, min(slc, count - lo))
+        times.append(t)
         outers.append(o)
         evals_l.append(e)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     clk = clocks.stop()
     launches = lib.trstmi_launch_count() - launches0
     t_local = sum(times)
-    tot_outer = sum(outers)
-    tot_evals = sum(evals_l)
+    tot_outer, tot_evals = sum(outers), sum(evals_l)
 
-    # cross-rank: max time, summed work, best mu + its frame (NCCL)
-    best_frame = None
+    # cross-rank: max time, summed work (torch.distributed); best-of through the product (NCCL)
     if world > 1:
         t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -287,45 +417,44 @@ def main():
         w = torch.tensor([tot_outer, tot_evals], dtype=torch.float64, device="cuda")
         dist.all_reduce(w)
         tot_outer_all, tot_evals_all = int(w[0].item()), int(w[1].item())
-        if sharded:  # the ranks processed one frame together
+        if sharded_frame:  # the ranks processed one frame together
             tot_outer_all, tot_evals_all = tot_outer, tot_evals
-        cand = torch.tensor([best_mu if best_mu is not None else float("inf"), float(first + best_trial)],
-                            dtype=torch.float64, device="cuda")
-        allc = [torch.empty_like(cand) for _ in range(world)]
-        dist.all_gather(allc, cand)
-        allc = [tuple(x.tolist()) for x in allc]
-        owner = min(range(world), key=lambda r: (allc[r][0], allc[r][1]))
-        fr = d_frames[best_trial].clone() if best_trial >= 0 else torch.zeros(dim, dtype=torch.float64, device="cuda")
-        dist.broadcast(fr, src=owner)
-        best_mu, gbest = allc[owner]
-        best_frame = fr
     else:
         t_all, tot_outer_all, tot_evals_all = t_local, tot_outer, tot_evals
-        gbest = first + best_trial
+    bmu, bidx = ctypes.c_double(), ctypes.c_int64()
+    d_win = torch.empty_like(d_best)
+    ctx.check(lib.trstmi_best_of_ranks(ctx.h, dim, best["mu"], best["trial"], ctypes.c_void_p(d_best.data_ptr()),
+                                       ctypes.c_void_p(d_win.data_ptr()), ctypes.byref(bmu), ctypes.byref(bidx), sptr),
+              "best_of_ranks")
 
-    # end-to-end through the C ABI with host buffers (H2D + D2H in the timed region)
-    e2e = None
-    if rank == 0 or world > 1:
-        h_params = starts.copy()
-        h_frames = np.empty_like(starts)
-        h_to = (abi.TrialOut * trials)()
-        h_so = (abi.StageOut * (trials * ns))()
-        e2e_times = []
-        for _ in range(1 if args.steps > 0 else 0):
-            h_params[:] = starts
-            rng = rng0.copy()
-            t0 = time.perf_counter()
-            rc = lib.trstmi_solve_batch(ctx.h, ctypes.byref(cfg), trials, ctypes.c_void_p(h_params.ctypes.data),
-                                        ctypes.c_void_p(rng.ctypes.data), ctypes.c_void_p(h_frames.ctypes.data),
-                                        ctypes.cast(h_to, ctypes.c_void_p), ctypes.cast(h_so, ctypes.c_void_p), None)
-            e2e_times.append(time.perf_counter() - t0)
-            ctx.check(rc, "solve_batch")
-        e2e_outer = sum(h_to[t].outer_iterations for t in range(trials))
-        if e2e_times:
-            e2e = {"value": e2e_outer / e2e_times[0] * (world if world > 1 else 1), "unit": "TR iterations/s",
-                   "h2d_bytes_per_step": int(starts.nbytes + rng0.nbytes),
-                   "d2h_bytes_per_step": int(2 * starts.nbytes + ctypes.sizeof(h_to) + ctypes.sizeof(h_so)
-                                              + rng0.nbytes)}
+    # end-to-end through the host-pointer C ABI: slice 0 again, H2D + D2H inside the timed region
+    cnt0 = min(slc, count)
+    h_params = starts[:cnt0].copy()
+    h_frames = np.empty_like(h_params)
+    h_to = (abi.TrialOut * cnt0)()
+    h_so = (abi.StageOut * (cnt0 * ns))()
+    rng = rng0[:cnt0].copy()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    rc = lib.trstmi_solve_batch(ctx.h, ctypes.byref(cfg), cnt0, ctypes.c_void_p(h_params.ctypes.data),
+                                ctypes.c_void_p(rng.ctypes.data), ctypes.c_void_p(h_frames.ctypes.data),
+                                ctypes.cast(h_to, ctypes.c_void_p), ctypes.cast(h_so, ctypes.c_void_p), None)
+    e2e_t = time.perf_counter() - t0
+    ctx.check(rc, "solve_batch")
+    e2e_outer = sum(h_to[t].outer_iterations for t in range(cnt0))
+    if world > 1:
+        w = torch.tensor([e2e_t, e2e_outer], dtype=torch.float64, device="cuda")
+        mx = w.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(w)
+        e2e_t_all, e2e_outer_all = mx[0].item(), (e2e_outer if sharded_frame else w[1].item())
+    else:
+        e2e_t_all, e2e_outer_all = e2e_t, e2e_outer
+    e2e = {"value": e2e_outer_all / e2e_t_all, "unit": "TR iterations/s",
+           "h2d_bytes_per_step": int(h_params.nbytes + rng.nbytes),
+           "d2h_bytes_per_step": int(2 * h_params.nbytes + ctypes.sizeof(h_to) + ctypes.sizeof(h_so) + rng.nbytes),
+           "what": "slice 0 (%d trials per rank) through trstmi_solve_batch with host buffers, wall clock" % cnt0}
 
     if rank != 0:
         if world > 1:
@@ -333,7 +462,7 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline: the anneal kernel is the only kernel of the step
+    # roofline: the anneal kernel is the only kernel of a step (profiles/)
     peak = ctypes.c_double()
     ctx.check(lib.trstmi_measure_dfma_peak(ctx.h, 20000, ctypes.byref(peak)), "dfma peak")
     achieved = tot_evals * fpe / t_local / 1e12
@@ -342,43 +471,41 @@ def main():
     if os.path.exists(prof):
         try:
             rec = json.load(open(prof)).get(args.config)
-            if rec:  # ncu dram read+write bytes per trial, scaled to this launch's trials
-                traffic = rec["bytes_per_trial"] * trials
+            if rec:  # ncu dram read+write bytes per trial, scaled to one step's trials
+                traffic = rec["bytes_per_trial"] * slc
         except Exception:
             traffic = None
 
     cpu = None
     if not args.no_cpu and world == 1:
-        threads = os.cpu_count() or 1
-        sample = args.cpu_trials or threads
-        cpu_outer = max_outer if workload == "anneal" else min(max_outer, args.cpu_outer or (1 if N > 2048 else 3))
-        s, o, e = cpu_sample(field, d, N, cpu_outer, sample, threads, workload=workload)
-        cpu = {"value": o / s, "unit": "TR iterations/s", "cores": min(sample, threads), "kind": "port",
-               "sample": "%d %s of this workload (trials 0..%d) on %d host threads, %.1f s; "
-                         "oracle/ CAS restatement (reference not buildable: no Eigen)"
-                         % (sample, "full anneals" if workload == "anneal" else
-                            "stage-0 runs capped at %d outer iterations" % cpu_outer, sample - 1, threads, s),
-               "gram_entries_per_s": e * n / s}
+        cpu = cpu_baseline(args, field, d, N, workload)
 
     value = tot_outer_all / t_all
     line = {
         "metric": METRIC, "value": value, "unit": "TR iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if (sharded_frame or args.scaling == "strong") else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "gram_entries_per_s": tot_evals_all * n / t_all, "evals_per_s": tot_evals_all / t_all,
-        "config": {"workload": "%s: %s lines d=%d N=%d, %d trials/GPU x %s(max_outer=%d, eps 1e-7, %d stage%s)"
-                   % (args.config, "complex" if field == abi.COMPLEX else "real", d, N, trials,
-                      "anneal" if workload == "anneal" else "anneal stage 0", max_outer, ns, "s" if ns > 1 else ""),
-                   "trials_per_gpu": trials, "max_outer": max_outer, "seed": 0,
-                   "l2": "flushed (256 MB write) before every timed step; inputs 13 MB",
-                   "parallelism": ("one frame, Gram row-blocks sharded over %d GPU(s) (NCCL)" % world) if sharded else
-                                  ("trials sharded over %d GPU(s), NCCL allgather(best mu)+broadcast(frame)" % world)},
-        "best_mu": best_mu, "best_trial": gbest,
+        "config": {"workload": "%s: %s lines d=%d N=%d, %d trials x %s(max_outer=%d, eps 1e-7, %d stage%s); "
+                               "step = full anneal of a %d-trial slice per rank"
+                   % (args.config, "complex" if field == abi.COMPLEX else "real", d, N, T,
+                      "anneal" if workload == "anneal" else "anneal stage 0", max_outer, ns, "s" if ns > 1 else "",
+                      slc),
+                   "trials": T, "trials_per_rank": count, "slice": slc, "max_outer": max_outer, "seed": 0,
+                   "l2": "flushed (256 MB write) before every timed step; trial state lives in shared memory",
+                   "parallelism": ("one frame, Gram row-blocks sharded over %d GPU(s) (NCCL)" % world)
+                   if sharded_frame else
+                   ("%s: trials in contiguous blocks over %d GPU(s); best-of by NCCL allgather(mu, trial) + "
+                    "broadcast(frame) (trstmi_best_of_ranks)" % (args.scaling, world))},
+        "best_mu": bmu.value, "best_trial": bidx.value,
         "welch_bound": api.welch_bound(d, N),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": achieved / peak.value, "traffic": traffic, "traffic_unit": "bytes/launch",
+                     "peak_nominal": NOMINAL_FP64_TFLOPS, "frac_nominal": achieved / NOMINAL_FP64_TFLOPS,
                      "note": "achieved = evals x (16|4)dN^2 (dense contraction count, SURVEY 8d) / step device time; "
-                             "peak = DFMA-loop throughput measured live on this GPU (MEASURED_PEAKS.json has no FP64)"},
+                             "peak = DFMA-loop throughput measured live on this GPU (MEASURED_PEAKS.json and "
+                             "B200_PROFILING.md have no FP64 figure); peak_nominal = 148 SM x 64 DFMA/clk x 1965 MHz"},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clk, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

@@ -238,6 +238,34 @@ int trstmi_solve(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restarts, uint6
                  double* best_frame, double* best_coherence, int64_t* best_restart, trstmi_trial_out* trial_out,
                  trstmi_stage_out* stage_out);
 
+/* ---- multi-GPU trial scheduler (solve()'s restart pool and
+ * best-of selection, solver.hpp:210-273, across one process per GPU) ----
+ * Restart i runs on rank floor(i * world / restarts): rank r owns the
+ * contiguous block [first, first + count). */
+int trstmi_shard_range(int64_t restarts, int world, int rank, int64_t* first, int64_t* count);
+/* Best-of rule of solve() (solver.hpp:256-263): the minimum mu over entries
+ * with ok != 0 (ok nullable = all) and mu not NaN, lowest index (index
+ * nullable = position) on ties.  ALL_FAILED when there is none. */
+int trstmi_select_best(int64_t n, const double* mu, const int64_t* index, const int32_t* ok, int64_t* best_pos);
+/* Attach an NCCL communicator (128-byte ncclUniqueId from
+ * trstmi_nccl_unique_id on rank 0, shared by the caller) to the context;
+ * world == 1 needs no id. */
+int trstmi_comm_init(trstmi_ctx* ctx, int world, int rank, const char* nccl_id);
+/* Cross-rank best-of: NCCL allgather of every rank's (local_mu, local_index)
+ * (NaN mu = no successful trial on that rank), selection by
+ * trstmi_select_best, then the owner broadcasts its frame (device pointers,
+ * dim doubles) into best_frame_dev on every rank. */
+int trstmi_best_of_ranks(trstmi_ctx* ctx, int64_t dim, double local_mu, int64_t local_index,
+                         const double* local_frame_dev, double* best_frame_dev, double* best_mu,
+                         int64_t* best_index, void* stream);
+/* solve() over the context's ranks: this rank's block of restarts
+ * (trstmi_shard_range) annealed on its GPU, then trstmi_best_of_ranks.  Every
+ * rank returns the same best frame / coherence / restart.  local_trial_out
+ * (nullable): the block's records (local_count entries). */
+int trstmi_solve_sharded(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restarts, uint64_t seed, double* best_frame,
+                         double* best_coherence, int64_t* best_restart, trstmi_trial_out* local_trial_out,
+                         int64_t* local_first, int64_t* local_count);
+
 /* Child seed of restart `index` (mix_seed, rng.hpp:13-18): RestartRecord::seed. */
 uint64_t trstmi_mix_seed(uint64_t seed, uint64_t index);
 

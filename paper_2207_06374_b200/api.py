@@ -83,6 +83,13 @@ def load_library():
     lib.trstmi_solve.argtypes = [vp, vp, c_i64, ctypes.c_uint64, c_i64, vp, vp, vp, vp, vp]
     lib.trstmi_nccl_unique_id.argtypes = [vp]
     lib.trstmi_set_shard.argtypes = [vp, c_int, c_int, vp]
+    lib.trstmi_shard_range.argtypes = [c_i64, c_int, c_int, vp, vp]
+    lib.trstmi_select_best.argtypes = [c_i64, vp, vp, vp, vp]
+    lib.trstmi_comm_init.argtypes = [vp, c_int, c_int, vp]
+    lib.trstmi_best_of_ranks.argtypes = [vp, c_i64, c_dbl, c_i64, vp, vp, vp, vp, vp]
+    lib.trstmi_solve_sharded.argtypes = [vp, vp, c_i64, ctypes.c_uint64, vp, vp, vp, vp, vp, vp]
+    lib.trstmi_launch_count.restype = ctypes.c_longlong
+    lib.trstmi_measure_dfma_peak.argtypes = [vp, c_int, vp]
     _lib = lib
     return lib
 

@@ -50,6 +50,18 @@ def sources():
     return out
 
 
+def _includes(path, seen=None):
+    """Transitive local #include "..." closure of a source file."""
+    import re
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    for m in re.finditer(r'^\s*#\s*include\s+"([^"]+)"', open(path).read(), re.M):
+        _includes(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen)
+    return seen
+
+
 def build(verbose=False, force=False, jobs=None):
     os.makedirs(BUILD, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
@@ -59,15 +71,18 @@ def build(verbose=False, force=False, jobs=None):
     jobs = jobs or max(2, min(8, os.cpu_count() or 2))
     tasks = []
     objs = []
+    me = [os.path.abspath(__file__)]
+
+    def add(src, o, extra):
+        objs.append(o)
+        if force or not _newer(o, sorted(_includes(src)) + me):  # per-object: only stale objects rebuild
+            tasks.append(COMMON + extra + ["-c", src, "-o", o])
+
     for cplx, s, g in INSTANCES:
         o = os.path.join(BUILD, "inst_%s_%d_%s.o" % ("c" if cplx else "r", s, "g" if g else "r"))
-        objs.append(o)
-        tasks.append(COMMON + ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-DINST_GS=%d" % g, "-c",
-                               os.path.join(CSRC, "instantiate.cu"), "-o", o])
-    for src in ("trstmi_capi.cu", "large_engine.cu", "analysis.cu"):
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
-        objs.append(o)
-        tasks.append(COMMON + ["-c", os.path.join(CSRC, src), "-o", o])
+        add(os.path.join(CSRC, "instantiate.cu"), o, ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-DINST_GS=%d" % g])
+    for src in ("trstmi_capi.cu", "large_engine.cu", "analysis.cu", "sharding.cu"):
+        add(os.path.join(CSRC, src), os.path.join(BUILD, src.replace(".cu", ".o")), [])
     with cf.ThreadPoolExecutor(jobs) as ex:
         for log in ex.map(lambda c: _run([NVCC] + c), tasks):
             if verbose and log.strip():

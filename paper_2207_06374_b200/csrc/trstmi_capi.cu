@@ -20,6 +20,7 @@
 #include "host/host_common.hpp"
 #include "kernel_table.hpp"
 #include "large_engine.hpp"
+#include "ctx.hpp"
 
 using namespace trstmi_dev;
 
@@ -70,17 +71,6 @@ __global__ void div_selftest_kernel(long long n, unsigned long long seed, unsign
   }
   if (nb) atomicAdd(bad, nb);
 }
-
-struct trstmi_ctx {
-  int device = 0;
-  int sm_count = 0;
-  cudaStream_t stream = nullptr;
-  int* counter = nullptr;
-  trstmi_large::Engine* large = nullptr;  // large-frame path engine (lazy)
-  int large_workers = 8;                  // concurrent large-path trials (streams)
-  int shard_world = 1;                    // single-frame row-block sharding (trstmi_set_shard)
-  std::string err;
-};
 
 // ------------------------------------------------------------------ path rule
 // Small-frame kernel choice for a shape: CTA width S (= the CAS reduction
@@ -361,6 +351,7 @@ int trstmi_ctx_destroy(trstmi_ctx* ctx) {
   if (!ctx) return TRSTMI_OK;
   cudaSetDevice(ctx->device);
   if (ctx->counter) cudaFree(ctx->counter);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->large) trstmi_large::engine_destroy(ctx->large);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

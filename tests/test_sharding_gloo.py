@@ -1,8 +1,10 @@
-"""Multi-rank trial sharding on CPU (gloo, world_size 2): shards partition
-the trial ids, and the best-of exchange (allgather + broadcast) returns the
-same (mu, id, frame) as the single-process selection — GPU-count invariance
-of solve()'s result (solver.hpp:256-267).  Per-trial anneals come from the
-oracle here (no GPU); on the box the same code runs over NCCL."""
+"""Multi-rank trial sharding on CPU (gloo, world_size 2): the product's
+partition (trstmi_shard_range) covers the trial ids in contiguous blocks, and
+the best-of exchange with the product's selection rule (trstmi_select_best)
+returns the same (mu, id, frame) as the single-process selection — GPU-count
+invariance of solve()'s result (solver.hpp:256-267).  Per-trial anneals come
+from the oracle here (no GPU); on the box trstmi_solve_sharded runs the same
+host logic over NCCL (tests/test_gpu_sharded.py)."""
 import os
 import socket
 
@@ -47,12 +49,23 @@ def _worker(rank, world, port, out):
 
 
 def test_shards_partition_trials():
-    for world in (1, 2, 3, 8):
-        ids = []
-        for r in range(world):
-            lo, hi = sharding.shard(4096, world, r)
-            ids.extend(range(lo, hi))
-        assert ids == list(range(4096))
+    for total in (1, 5, 64, 1000, 4096):
+        for world in (1, 2, 3, 8):
+            ids = []
+            for r in range(world):
+                lo, hi = sharding.shard(total, world, r)
+                assert all(i * world // total == r for i in range(lo, hi))  # trial i on rank floor(i G / T)
+                ids.extend(range(lo, hi))
+            assert ids == list(range(total))
+
+
+def test_select_best_rule():
+    # strict < in index order: the lowest index wins ties; failed / NaN entries are skipped
+    assert sharding.select_best([0.5, 0.4, 0.4, 0.7]) == 1
+    assert sharding.select_best([0.5, 0.4, 0.4], ids=[9, 7, 3]) == 2
+    assert sharding.select_best([0.1, 0.4, 0.3], ok=[0, 1, 1]) == 2
+    assert sharding.select_best([float("nan"), 0.4]) == 1
+    assert sharding.select_best([float("nan")]) == -1
 
 
 def test_two_rank_best_equals_single_process():
