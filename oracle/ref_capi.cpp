@@ -106,12 +106,15 @@ struct Trial {
   Counters cnt;
   std::int64_t outer = 0;
   int status = 0;  // 0 ok, 1 zero column escaped, 2 other exception
+  std::vector<OuterRecord> history;  // kept when the batch records (ref_batch_keep_history)
+  std::vector<int> history_stage;
 };
 
 struct Batch {
   int field;
   Index d, N;
   std::vector<Trial> trials;
+  bool keep_history = false;
 };
 
 template <class F>
@@ -267,6 +270,11 @@ double ref_batch_run_stages(void* h, const double* schedule, int n_stages, int k
                                                    std::move(tr.param), trc);
         tr.param = std::move(res.x);
         tr.outer += (std::int64_t)res.history.size();
+        if (b->keep_history)
+          for (const OuterRecord& r : res.history) {
+            tr.history.push_back(r);
+            tr.history_stage.push_back(k);
+          }
         if (stage_rec) {
           double* r = stage_rec + (t * n_stages + k) * 4;
           r[0] = schedule[k];
@@ -292,6 +300,33 @@ double ref_batch_run_stages(void* h, const double* schedule, int n_stages, int k
   if (evals) *evals = e;
   if (hvps) *hvps = hv;
   return sec;
+}
+
+void ref_batch_keep_history(void* h, int on) { static_cast<Batch*>(h)->keep_history = on != 0; }
+
+// OuterRecords (trust_region.hpp:163-173) of trial t, at most cap, as
+// trstmi_outer_out-shaped rows: {stage, iteration, cg_exit, cg_iterations,
+// accepted} ints + {value, grad_norm, radius, rho, step_norm} doubles.
+// Returns the number of records the trial has.
+std::int64_t ref_batch_history(void* h, std::int64_t t, std::int64_t cap, int* ints5, double* dbl5) {
+  const Trial& tr = static_cast<Batch*>(h)->trials[t];
+  const std::int64_t n = (std::int64_t)tr.history.size();
+  for (std::int64_t i = 0; i < n && i < cap; ++i) {
+    const OuterRecord& r = tr.history[i];
+    int* o = ints5 + 5 * i;
+    o[0] = tr.history_stage[i];
+    o[1] = r.iteration;
+    o[2] = static_cast<int>(r.cg_exit);
+    o[3] = r.cg_iterations;
+    o[4] = r.accepted ? 1 : 0;
+    double* v = dbl5 + 5 * i;
+    v[0] = r.value;
+    v[1] = r.grad_norm;
+    v[2] = r.radius;
+    v[3] = r.rho;
+    v[4] = r.step_norm;
+  }
+  return n;
 }
 
 // Raw parameters (count x dim) and per-trial status of the batch.

@@ -40,6 +40,9 @@ def lib():
         L.ref_batch_run_stages.argtypes = [vp, vp, c_int, c_int, c_int, vp, vp, c_int, vp, vp, vp, vp]
         L.ref_batch_run_stages.restype = dbl
         L.ref_batch_params.argtypes = [vp, vp, vp]
+        L.ref_batch_keep_history.argtypes = [vp, c_int]
+        L.ref_batch_history.argtypes = [vp, i64, i64, vp, vp]
+        L.ref_batch_history.restype = i64
         L.ref_anneal.argtypes = [i64, i64, vp, c_int, vp, vp, u64, i64, vp, vp, vp]
         L.ref_solve.argtypes = [i64, i64, c_int, u64, dbl, vp, vp, c_int, vp, vp, vp, vp, vp]
         _lib = L
@@ -116,6 +119,18 @@ class Batch:
         sec = lib().ref_batch_run_stages(self.h, _p(self.sched), self.ns, k0, k1, _p(self.tr6), _p(self.tri), threads,
                                          _p(self.rec), ctypes.byref(o), ctypes.byref(e), ctypes.byref(hv))
         return sec, o.value, e.value, hv.value
+
+    def keep_history(self, on=True):
+        lib().ref_batch_keep_history(self.h, int(on))
+
+    def history(self, t, cap=100000):
+        """OuterRecords of trial t: (ints[:, stage, iteration, cg_exit, cg_iterations, accepted],
+        doubles[:, value, grad_norm, radius, rho, step_norm])."""
+        ints = np.zeros((cap, 5), np.int32)
+        dbl = np.zeros((cap, 5))
+        n = lib().ref_batch_history(self.h, t, cap, _p(ints), _p(dbl))
+        n = min(n, cap)
+        return ints[:n], dbl[:n]
 
     def params(self):
         out = np.empty((self.count, _dim(self.cfg.field, self.cfg.d, self.cfg.N)))
