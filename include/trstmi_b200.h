@@ -153,7 +153,8 @@ long long trstmi_launch_count(void);
 /* FP64 roofline denominator: measured DFMA throughput of the device (TFLOP/s). */
 int trstmi_measure_dfma_peak(trstmi_ctx* ctx, int iters, double* tflops);
 
-/* Self tests: device CAS exp (which = 0) / log (1) on host arrays, and the
+/* Self tests: device CAS exp (which = 0) / log (1) on host arrays (hypot (2):
+ * x holds n (re, im) pairs, y receives n magnitudes), and the
  * Markstein division used by the kernels vs IEEE division on n seeded pairs. */
 int trstmi_selftest_cas_math(trstmi_ctx* ctx, int which, const double* x, double* y, int64_t n);
 int trstmi_selftest_division(trstmi_ctx* ctx, int64_t n, uint64_t seed, uint64_t* mismatches);

@@ -143,6 +143,47 @@ inline double cas_exp(double x) {
 // CAS log (used once per evaluation, for F = s + delta*log z with z >= 1):
 // x = 2^e m, m in [sqrt(1/2), sqrt(2)), log m = 2 atanh(f/(2+f)) by an odd
 // series in Horner/fma form, plus e*ln2 split hi/lo.
+// |re + i im| for coherence / offdiagonal_magnitudes: std::abs(complex) is
+// glibc's hypot (frame.hpp:87).  Restatement of glibc 2.39 __hypot
+// (sysdeps/ieee754/dbl-64/e_hypot.c, the non-FMA correction kernel of Borges,
+// "An Improved Algorithm for hypot(a,b)", with the 2^-600 scaling);
+// -ffp-contract=off keeps every operation separately rounded.  Mirrors
+// cas_hypot in csrc/cas_math.cuh.
+inline double cas_hypot_kernel(double ax, double ay) {
+  double h = std::sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= 2.0 * ay) {
+    const double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    const double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+
+inline double cas_hypot(double x, double y) {
+  x = std::fabs(x);
+  y = std::fabs(y);
+  if (std::isinf(x) || std::isinf(y)) return std::numeric_limits<double>::infinity();
+  if (std::isnan(x) || std::isnan(y)) return x + y;
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  const double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+  if (ax > kLarge) {
+    if (ay <= ax * kEps) return ax + ay;
+    return cas_hypot_kernel(ax * kScale, ay * kScale) / kScale;
+  }
+  if (ay < kTiny) {
+    if (ax >= ay / kEps) return ax + ay;
+    return cas_hypot_kernel(ax / kScale, ay / kScale) * kScale;
+  }
+  if (ay <= ax * kEps) return ax + ay;
+  return cas_hypot_kernel(ax, ay);
+}
+
 inline double cas_log(double x) {
   if (!(x == x) || x < 0.0) return std::numeric_limits<double>::quiet_NaN();
   if (x == 0.0) return -std::numeric_limits<double>::infinity();
@@ -420,7 +461,7 @@ inline CoherenceResult coherence(const Shape& sh, const double* frame, bool norm
     for (std::int64_t k = j + 1; k < N; ++k, ++p) {
       double gr, gi;
       gram_entry(sh, &phi[j * L], &phi[k * L], &gr, &gi);
-      const double m = std::sqrt(gr * gr + gi * gi);
+      const double m = cas_hypot(gr, gi);  // std::abs = hypot (frame.hpp:87)
       if (m > r.mu) {
         r.mu = m;
         r.argmax = p;
@@ -471,6 +512,7 @@ inline HvpResult hvp_adapter(const Shape& sh, const Vec& x, const Vec& dir, doub
     }
     Vec g0;
     if (g0_in) g0 = *g0_in; else { g0 = eval_objective(sh, x.data(), nullptr, 0.0, delta).grad; r.evals++; }
+    r.evals++;  // solver.hpp:130 re-evaluates x + h*dir (the value of gp)
     for (std::int64_t i = 0; i < dim; ++i) r.hv[i] = (gp.grad[i] - g0[i]) / h;
     r.path = HVP_FORWARD;
     return r;

@@ -146,6 +146,7 @@ void orc_exp_array(const double* x, double* y, std::int64_t n) {
 void orc_log_array(const double* x, double* y, std::int64_t n) {
   for (std::int64_t i = 0; i < n; ++i) y[i] = cas_log(x[i]);
 }
+double orc_hypot(double x, double y) { return cas_hypot(x, y); }
 double orc_cas_sum(const double* v, std::int64_t n, int S) { return cas_sum(v, n, S); }
 double orc_cas_dot(const double* a, const double* b, std::int64_t n, int S) { return cas_dot(a, b, n, S); }
 std::uint64_t orc_mix_seed(std::uint64_t seed, std::uint64_t index) { return mix_seed(seed, index); }
@@ -284,7 +285,7 @@ void orc_offdiag_magnitudes(int field, std::int64_t d, std::int64_t N, const dou
     for (std::int64_t k = j + 1; k < N; ++k, ++p) {
       double gr, gi;
       gram_entry(sh, frame + j * L, frame + k * L, &gr, &gi);
-      mags[p] = std::sqrt(gr * gr + gi * gi);
+      mags[p] = cas_hypot(gr, gi);
     }
 }
 

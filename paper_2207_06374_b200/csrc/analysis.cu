@@ -78,7 +78,7 @@ __global__ void an_magnitudes(const double* __restrict__ f, int cplx, int d, int
     } else {
       for (int i = 0; i < d; ++i) re = fma(a[i], c[i], re);
     }
-    mags[p] = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+    mags[p] = cas_hypot(re, im);  // std::abs = hypot (frame.hpp:87)
   }
 }
 
@@ -105,7 +105,7 @@ __global__ void an_frame_operator(const double* __restrict__ f, int cplx, int d,
       }
     }
     if (r == s) re = __dsub_rn(re, (double)N / (double)d);
-    m = sqrt(__dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)));
+    m = cas_hypot(re, im);
   }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));

@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
                 if (zm < 0) {
                   const double h2 = 2.0 * h;
                   for (int i = tid; i < dim; i += S) bd[i] = (bd[i] - gt[i]) / h2;
-                } else {  // forward fallback: (g(x+hd) - g0)/h, g0 == current gradient
-                  ++evals;
+                } else {  // forward fallback: (g(x+hd) - g0)/h; the reference evaluates g0 and
+                  evals += 2;  // g(x+hd) again (solver.hpp:129-130): g0 == current gradient, g(x+hd) reused
                   for (int i = tid; i < dim; i += S) bd[i] = (bd[i] - g[i]) / h;
                 }
               } else {  // x+hd hit a zero column: g0, retry forward (fails again), backward

@@ -90,6 +90,8 @@ Engine* engine_create(int device, cudaStream_t stream) {
   return E;
 }
 
+void engine_set_stream(Engine* E, cudaStream_t stream) { E->st = stream; }
+
 static void free_work(Work& w) {
   double** ptrs[] = {&w.phiT, &w.alpha, &w.X, &w.GR, &w.GI, &w.zpart, &w.scal, &w.PR, &w.PI, &w.CU,
                      &w.part, &w.tpart, &w.tile_mu, &w.x, &w.g, &w.zs, &w.r, &w.dv, &w.bd, &w.xt,
@@ -193,19 +195,28 @@ static LargeEval make_eval_w(Work& w, const Shape& sh, const double* x, const do
   return L;
 }
 
+// Dynamic shared-memory opt-in of `fn` on the current device (the attribute is
+// per function and per device; cached per (function, device), failures are
+// not cached).
+static cudaError_t ensure_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{fn, dev}];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 // K1 with its staging buffer (norm_smem(L) bytes of dynamic shared memory)
 static cudaError_t launch_normalize(const LargeEval& L, cudaStream_t st) {
   const size_t bytes = norm_smem(L.L);
-  static size_t set = 0;  // largest opt-in so far (the attribute is per function, not per stream)
-  static std::mutex mu;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (bytes > set) {
-      const cudaError_t e = cudaFuncSetAttribute(large_normalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      if (e != cudaSuccess) return e;
-      set = bytes;
-    }
-  }
+  const cudaError_t e = ensure_smem((const void*)large_normalize, bytes);
+  if (e != cudaSuccess) return e;
   const int nc = norm_cols(L.L);
   large_normalize<<<(L.N + nc - 1) / nc, NORM_THREADS, bytes, st>>>(L);
   return cudaGetLastError();
@@ -215,12 +226,7 @@ static cudaError_t launch_normalize(const LargeEval& L, cudaStream_t st) {
 // 32-column CTAs for small frames (twice the CTAs of a single-wave grid)
 template <bool CPLX, int GMT>
 static cudaError_t launch_grad_gemm_t(const LargeEval& L, int cols, int d, int K, cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(large_grad_gemm<CPLX, GMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)gg_smem(GMT));
-  });
+  const cudaError_t attr = ensure_smem((const void*)large_grad_gemm<CPLX, GMT>, gg_smem(GMT));
   if (attr != cudaSuccess) return attr;
   dim3 gg((cols + GMT - 1) / GMT, (d + GRB - 1) / GRB, K);
   large_grad_gemm<CPLX, GMT><<<gg, 256, gg_smem(GMT), st>>>(L);
@@ -704,8 +710,8 @@ int anneal_trial(Engine* E, const Shape& sh, const TrCfg& tr, const std::vector<
               if ((rc = eval(E, sh, x, w.dv, -h, delta, 1, w.gm, &Fx, &sx, nullptr, &zm, err))) return rc;
               if (zm < 0) {
                 large_fd<<<G, 256, 0, st>>>(w.bd, w.gp, w.gm, 2.0 * h, dim);
-              } else {
-                ++evals;
+              } else {  // forward fallback: g0 and g(x + h d) again (solver.hpp:129-130), reused values
+                evals += 2;
                 large_fd<<<G, 256, 0, st>>>(w.bd, w.gp, g, h, dim);
               }
             } else {

@@ -33,6 +33,7 @@ bool use_large(int field, long long d, long long N);
 struct Engine;
 Engine* engine_create(int device, cudaStream_t stream);
 void engine_destroy(Engine*);
+void engine_set_stream(Engine* E, cudaStream_t stream);
 
 // Row-block sharding of a single frame over `world` ranks.
 // nccl_id == NULL: virtual ranks, all shares computed on this device (tests);

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256) large_gram(LargeEval E, double* tile_mu, 
           if (CPLX) E.GI[p] = im[a][b];
           best = fmax(best, xv);
         } else {
-          const double m = sqrt(u);
+          const double m = cas_hypot(re[a][b], CPLX ? im[a][b] : 0.0);  // std::abs (frame.hpp:87)
           if (m > best || (m == best && m > 0.0 && p < barg)) {
             best = m;
             barg = p;

@@ -752,7 +752,7 @@ __device__ int coherence_cta(const Prob& P, const double* __restrict__ f, bool n
     for (int u = 0; u < 4; ++u) gram_jk<CPLX, DMAX, EXACT>(sm.phiS, N, d, j[u], k[u], re[u], im[u]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double m = sqrt(CPLX ? __dadd_rn(__dmul_rn(re[u], re[u]), __dmul_rn(im[u], im[u])) : __dmul_rn(re[u], re[u]));
+      const double m = cas_hypot(re[u], CPLX ? im[u] : 0.0);  // std::abs = hypot (frame.hpp:87)
       if (v[u] && m > best) {  // pairs ascend within a thread: first strict maximum
         best = m;
         arg = p[u];

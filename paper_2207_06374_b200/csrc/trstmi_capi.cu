@@ -45,7 +45,7 @@ __global__ void dfma_peak_kernel(double* out, int iters, double a, double b) {
 // Markstein division against the hardware IEEE division on a seeded stream.
 __global__ void cas_math_kernel(const double* x, double* y, long long n, int which) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    y[i] = which == 0 ? cas_exp(x[i]) : cas_log(x[i]);
+    y[i] = which == 0 ? cas_exp(x[i]) : which == 1 ? cas_log(x[i]) : cas_hypot(x[2 * i], x[2 * i + 1]);
 }
 
 __device__ __forceinline__ unsigned long long sm64(unsigned long long& s) {
@@ -224,11 +224,12 @@ int trstmi_selftest_cas_math(trstmi_ctx* ctx, int which, const double* x, double
   if (!ctx || n < 0) return TRSTMI_ERR_INVALID_ARG;
   cudaSetDevice(ctx->device);
   DBuf dx, dy;
-  CUDA_TRY(ctx, cudaMalloc(&dx.p, std::max<int64_t>(n, 1) * 8));
+  const int64_t nin = which == 2 ? 2 * n : n;  // hypot: n (x, y) pairs
+  CUDA_TRY(ctx, cudaMalloc(&dx.p, std::max<int64_t>(nin, 1) * 8));
   CUDA_TRY(ctx, cudaMalloc(&dy.p, std::max<int64_t>(n, 1) * 8));
   // every copy on the context's (non-blocking) stream: a legacy-stream
   // cudaMemcpy is not ordered with it and may still be in flight
-  CUDA_TRY(ctx, cudaMemcpyAsync(dx.p, x, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(dx.p, x, nin * 8, cudaMemcpyHostToDevice, ctx->stream));
   cas_math_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>((const double*)dx.p, (double*)dy.p, n, which);
   CUDA_TRY(ctx, cudaGetLastError());
   CUDA_TRY(ctx, cudaMemcpyAsync(y, dy.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -368,8 +369,12 @@ static int large_workers(const trstmi_ctx* ctx) {
   return v > 0 ? v : ctx->large_workers;
 }
 
+// The context's large-frame engine, bound to the stream of the current call
+// (every entry point passes its own: the caller's for *_dev, else ctx->stream,
+// which also carries that call's H2D copies).
 static trstmi_large::Engine* large_engine(trstmi_ctx* ctx, cudaStream_t st) {
   if (!ctx->large) ctx->large = trstmi_large::engine_create(ctx->device, st);
+  trstmi_large::engine_set_stream(ctx->large, st);
   return ctx->large;
 }
 

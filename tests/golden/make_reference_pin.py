@@ -18,7 +18,8 @@ Stored per (config, delta):
     coherence mu of the frame and its first-argmax pair;
   * cas: sha256 of the CAS oracle's F, s and gradient bits (the bit-level
     contract the GPU must meet) and the CAS F, s;
-  * hvp (configs 1-4, direction r_0 scaled to unit norm): reference
+  * hvp (configs 1-4, direction r_0 / 256 — an exact scaling, so every
+    platform forms the same input bits): reference
     |Hv| and 128 samples, CAS sha256.
 """
 import hashlib
@@ -103,7 +104,7 @@ def main(only=None):
             e["cas_vs_ref"] = {"F_rel": rel, "grad_rel_l2": float(grel),
                                "grad_componentwise": float(np.max(np.abs(g - go) / np.maximum(np.abs(g), 1.0)))}
             if N <= 1024:
-                v = rs[0] / np.linalg.norm(rs[0])
+                v = rs[0] * 0.00390625  # exact power-of-two scaling: no platform-dependent norm in the input
                 hv, hz = R.hvp(field, d, N, x, v, delta)
                 ho, path, hoz = O.hvp(field, d, N, S, x, v, delta)
                 e["hvp"] = {"ref_norm": float(np.linalg.norm(hv)), "ref_samples": hv[idx].tolist(),

@@ -34,6 +34,8 @@ def lib():
         L.orc_log.argtypes = [dbl]
         L.orc_log.restype = dbl
         L.orc_exp_array.argtypes = [vp, vp, i64]
+        L.orc_hypot.argtypes = [dbl, dbl]
+        L.orc_hypot.restype = dbl
         L.orc_log_array.argtypes = [vp, vp, i64]
         L.orc_cas_sum.argtypes = [vp, i64, c_int]
         L.orc_cas_sum.restype = dbl
@@ -72,6 +74,11 @@ def exp(x):
     y = np.empty_like(x)
     lib().orc_exp_array(_p(x), _p(y), x.size)
     return y
+
+
+def hypot(x, y):
+    f = np.frompyfunc(lib().orc_hypot, 2, 1)
+    return np.asarray(f(np.asarray(x, np.float64), np.asarray(y, np.float64)), np.float64)
 
 
 def log(x):

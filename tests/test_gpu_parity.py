@@ -211,6 +211,24 @@ def test_device_cas_math_bit_identical_to_oracle(ctx):
     w = np.empty_like(z)
     assert lib.trstmi_selftest_cas_math(ctx.h, 1, z.ctypes.data, w.ctypes.data, z.size) == 0
     assert np.array_equal(w.view(np.uint64), orc.log(z).view(np.uint64))
+    # hypot (coherence magnitudes, frame.hpp:87): device == oracle == the host libm, bit for bit
+    pr = hypot_inputs(rng, 300000)
+    h = np.empty(pr.shape[0])
+    assert lib.trstmi_selftest_cas_math(ctx.h, 2, pr.ctypes.data, h.ctypes.data, pr.shape[0]) == 0
+    assert np.array_equal(h.view(np.uint64), orc.hypot(pr[:, 0], pr[:, 1]).view(np.uint64))
+    assert np.array_equal(h.view(np.uint64), np.hypot(pr[:, 0], pr[:, 1]).view(np.uint64))
+
+
+def hypot_inputs(rng, n):
+    """(x, y) pairs: coherence-range magnitudes plus the whole exponent range,
+    zeros, infinities and NaN."""
+    e1 = rng.integers(-1070, 1020, n)
+    e2 = np.clip(e1 + rng.integers(-60, 60, n), -1074, 1020)
+    a = rng.uniform(-1, 1, n) * np.ldexp(1.0, e1)
+    b = rng.uniform(-1, 1, n) * np.ldexp(1.0, e2)
+    m = rng.uniform(-1, 1, (n, 2))
+    special = np.array([[0.0, 0.0], [-0.0, 3.0], [np.inf, np.nan], [np.nan, 1.0], [1e-320, 1e-321], [1e308, 1e308]])
+    return np.ascontiguousarray(np.concatenate([np.stack([a, b], 1), m, special]))
 
 
 def test_markstein_division_matches_ieee(ctx):

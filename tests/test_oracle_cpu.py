@@ -23,6 +23,15 @@ def test_ported_reference_unit_tests():
     assert "0 failures" in r.stdout
 
 
+def test_cas_hypot_matches_libm():
+    """CAS |G| for coherence is glibc's hypot restated (std::abs(complex),
+    frame.hpp:87): bit-identical to this host's libm over the exponent range."""
+    from tests.test_gpu_parity import hypot_inputs
+    pr = hypot_inputs(np.random.default_rng(11), 400000)
+    h = orc.hypot(pr[:, 0], pr[:, 1])
+    assert np.array_equal(h.view(np.uint64), np.hypot(pr[:, 0], pr[:, 1]).view(np.uint64))
+
+
 def test_cas_exp_accuracy_vs_mpmath():
     mpmath = pytest.importorskip("mpmath")
     mpmath.mp.prec = 160
