@@ -1,0 +1,728 @@
+// Batched device engine (BDE) for large frames (BASELINE configs 4-5 and any
+// shape whose trial state does not fit one SM): many evaluation requests —
+// the trust-region points of every trial in flight, or the B points of an
+// eval/hvp/coherence batch — run through ONE launch per pipeline kernel
+// (request index in the grid), and the trust-region / Steihaug-CG / anneal
+// control of every trial runs on the device (bde_tr.cuh).
+//
+// Pipeline (one launch each, all requests of a tick):
+//   bde_normalize   alpha_j, phi = p / alpha in the point layout (column j =
+//                   L contiguous doubles), first zero column
+//   bde_gram        upper-triangular 64x64 Gram tiles on the FP64 tensor
+//                   cores (mma.sync m16n8k4 .f64 = DMMA): complex products as
+//                   one real GEMM over the interleaved K = 2d with operands
+//                   R and J R; the epilogue keeps only G(j,k), j < k, packed
+//                   (interleaved re, im) and the block max of x = |G|^2
+//   bde_weights     w = exp((x - s)/delta) (x recomputed from G), z partial
+//                   per 16-row block
+//   bde_zreduce     z in block order, F = s + delta log z
+//   bde_grad        D^T = P^T Phi on DMMA with the coefficient matrix
+//                   P(k, m) = (w/z) G(k, m) (conjugated below the diagonal)
+//                   formed tile by tile in shared memory from the packed
+//                   (w, G) — the N x N coefficient matrix never exists in HBM
+//                   (north star: W o G fused into the contraction) — plus the
+//                   t chunk partials sum_k (w/z) u
+//   bde_finalize    chunk partials left to right, grad = ((acc - t phi)/alpha) 2
+//
+// Arithmetic: the Canonical Arithmetic Spec of the large path,
+// bit for bit.  DMMA computes each output as the ascending fma chain over its
+// k inputs (measured: profiles/r2_dmma_probe.txt — 0 mismatches against
+// std::fma chains on 1.8 M outputs), so a DMMA GEMM over the interleaved
+// complex layout reproduces the CAS Gram order (re: ar br, ai bi; im: ar bi,
+// -ai br per i ascending) and gradient order (re: fr pr, -fi pi; im: fr pi,
+// fi pr per k ascending within a chunk) exactly; every other operation is the
+// same IEEE operation as in large_path.cuh / the oracle.
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "small_path.cuh"
+
+namespace trstmi_bde {
+using namespace trstmi_dev;
+
+constexpr int BT = 64;            // Gram tile edge / gradient m-block
+constexpr int BZROWS = 16;        // CAS z blocks (rows) — as large_path.cuh ZROWS
+constexpr int BZLANES = 256;      // CAS z lanes per block
+constexpr int GKS = 32;           // Gram: K (interleaved) per pipeline stage
+constexpr int GSA = GKS + 4;      // Gram smem row stride (== 4 mod 16: conflict-free fragments)
+constexpr int NORM_T = 128;
+
+struct Shape {
+  int cplx, d, N, L, dim, K;  // L = 2d (complex) / d (real); K = CAS gradient chunks
+  long long n;                // pairs
+  int nt, tiles, nzb;         // 64-tiles per side, upper tiles, z blocks
+};
+
+enum ReqKind { REQ_OBJ = 0, REQ_COH_NORM = 1, REQ_COH_RAW = 2 };
+
+// One evaluation request: the point x + sc * dir (dir nullable).
+struct Req {
+  const double* x;
+  const double* dir;
+  double sc;
+  double delta;
+  double* grad;   // REQ_OBJ: dim doubles out
+  double* wout;   // nullable: softmax weights (n) out
+  int kind;
+  int squared;
+  int slot;       // workspace slot
+  int pad;
+};
+
+struct ReqOut {
+  double F, s, z, mu;
+  long long argmax;
+  unsigned long long smax;  // bits of max x (x >= 0)
+  int zc;                   // first zero column (INT_MAX: none)
+  int pad;
+};
+
+// Slot-strided workspace.
+struct Ws {
+  double* phi;    // dim per slot, point layout
+  double* alpha;  // N
+  double* G;      // n (real) / 2n (complex, interleaved)
+  double* W;      // n
+  double* zpart;  // nzb
+  double* part;   // K x dim
+  double* tpart;  // K x N
+  double* tmu;    // tiles
+  long long* targ;
+  long long s_phi, s_alpha, s_G, s_W, s_zpart, s_part, s_tpart, s_tile;
+};
+
+struct Pipe {
+  Shape sh;
+  const Req* reqs;
+  ReqOut* outs;   // indexed by request
+  const int* active;  // request ids of this launch (blockIdx.y / .z -> active[.])
+  Ws ws;
+};
+
+__device__ __forceinline__ long long pair_index(long long j, long long k, long long N) {
+  return j * N - j * (j + 1) / 2 + (k - j - 1);
+}
+
+__device__ __forceinline__ void tile_coords(int t, int nt, int& jb, int& kb) {
+  // upper-triangular tile t (row-major over jb <= kb)
+  int row = 0, rem = t;
+  while (rem >= nt - row) {
+    rem -= nt - row;
+    ++row;
+  }
+  jb = row;
+  kb = row + rem;
+}
+
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa16(double* dst, const double* src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NP>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NP) : "memory"); }
+
+// D (m16 x n8, f64) += A (m16 x k4) B (k4 x n8): one DMMA, the ascending fma
+// chain over k per output.  a0 = A[g][t], a1 = A[g+8][t], b = B[t][g];
+// c0,c1 = C[g][2t, 2t+1], c2,c3 = C[g+8][2t, 2t+1]  (g = lane/4, t = lane%4).
+__device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, double b) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b));
+}
+
+// ---------------------------------------------------------------- K1
+// A CTA normalises NC consecutive columns (one contiguous run of NC*L doubles
+// of the point), CAS norm chain per column, Markstein quotients (== IEEE).
+__host__ __device__ inline int bde_norm_cols(int L) { return max(1, min(32, 2048 / (L + 1))); }
+__host__ __device__ inline size_t bde_norm_smem(int L) {
+  return ((size_t)bde_norm_cols(L) * (L + 1) + 2 * (size_t)bde_norm_cols(L)) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(NORM_T) bde_normalize(Pipe P) {
+  extern __shared__ double ncol[];  // NC x (L + 1), then alpha[NC], 1/alpha[NC]
+  const Shape& sh = P.sh;
+  const int r = P.active[blockIdx.y];
+  const Req q = P.reqs[r];
+  const int L = sh.L, LP = L + 1, NC = bde_norm_cols(L);
+  double* sal = ncol + NC * LP;
+  double* sya = sal + NC;
+  const int j0 = blockIdx.x * NC;
+  const int nc = min(NC, sh.N - j0);
+  const long long base = (long long)j0 * L;
+  double* phi = P.ws.phi + (long long)q.slot * P.ws.s_phi;
+  const bool raw = q.kind == REQ_COH_RAW;
+  for (int e0 = 0; e0 < nc * L; e0 += 8 * NORM_T) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * NORM_T + threadIdx.x;
+      double xv = 0.0;
+      if (e < nc * L) {
+        xv = q.x[base + e];
+        if (q.sc != 0.0) xv = __dadd_rn(xv, __dmul_rn(q.sc, q.dir[base + e]));
+      }
+      v[u] = xv;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * NORM_T + threadIdx.x;
+      if (e < nc * L) {
+        if (raw) {
+          phi[base + e] = v[u];
+        } else {
+          const int c = e / L, qq = e - c * L;
+          ncol[c * LP + qq] = v[u];
+        }
+      }
+    }
+  }
+  if (raw) return;
+  __syncthreads();
+  double* alpha = P.ws.alpha + (long long)q.slot * P.ws.s_alpha;
+  for (int c = threadIdx.x; c < nc; c += NORM_T) {
+    const double* col = ncol + c * LP;
+    double acc = 0.0;
+    for (int qq = 0; qq < L; ++qq) acc = fma(col[qq], col[qq], acc);
+    const double a = sqrt(acc);
+    alpha[j0 + c] = a;
+    sal[c] = a;
+    sya[c] = __drcp_rn(a);
+    if (a < kZeroColumnTol) atomicMin(&P.outs[r].zc, j0 + c);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nc * L; e += NORM_T) {  // coalesced point-layout stores
+    const int c = e / L, qq = e - c * L;
+    phi[base + e] = div_rn(ncol[c * LP + qq], sal[c], sya[c]);
+  }
+}
+
+// ---------------------------------------------------------------- K2
+// Upper-triangular 64x64 tile (jb <= kb) of G = Phi* Phi on DMMA.  8 warps:
+// warp (wj, wk) = (w / 4, w % 4) owns rows 32 wj .. +32 and columns 16 wk ..
+// +16: two m16 x two n8 MMA tiles, re (and im) accumulators.  Operands are
+// the columns of phi (rows of R^T), staged through shared memory by
+// cp.async in GKS-wide K stages, two buffers.
+// MODE 0: objective (packed G, block max of x); MODE 1: coherence (|G| by
+// hypot, first argmax of the tile).
+__host__ __device__ constexpr size_t bde_gram_smem() { return 2 * 2 * (size_t)BT * GSA * sizeof(double); }
+
+template <bool CPLX, int MODE>
+__global__ void __launch_bounds__(256, 2) bde_gram(Pipe P) {
+  extern __shared__ __align__(16) double gsm[];  // [buf][A | B][64][GSA]
+  __shared__ double red_v[8];
+  __shared__ long long red_i[8];
+  const Shape& sh = P.sh;
+  const int r = P.active[blockIdx.y];
+  const Req q = P.reqs[r];
+  if (P.outs[r].zc != INT_MAX && q.kind != REQ_COH_RAW) return;  // zero column: nothing to compute
+  const int N = sh.N, L = sh.L;
+  int jb, kb;
+  tile_coords(blockIdx.x, sh.nt, jb, kb);
+  const double* phi = P.ws.phi + (long long)q.slot * P.ws.s_phi;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wj = warp >> 2, wk = warp & 3;
+  double re[2][2][4], im[2][2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) re[a][b][e] = im[a][b][e] = 0.0;
+  const int nst = (L + GKS - 1) / GKS;
+  auto issue = [&](int s, int buf) {
+    if (s < nst) {
+      double* As = gsm + buf * (2 * BT * GSA);
+      double* Bs = As + BT * GSA;
+      const int q0 = s * GKS;
+      for (int e = tid; e < BT * GKS; e += 256) {
+        const int row = e / GKS, c = e - row * GKS;
+        const int qq = q0 + c;
+        const int j = jb * BT + row, k = kb * BT + row;
+        const bool vq = qq < L;
+        cpa8(As + row * GSA + c, phi + (vq && j < N ? (long long)j * L + qq : 0), vq && j < N);
+        cpa8(Bs + row * GSA + c, phi + (vq && k < N ? (long long)k * L + qq : 0), vq && k < N);
+      }
+    }
+    cpa_commit();
+  };
+  issue(0, 0);
+  for (int s = 0; s < nst; ++s) {
+    issue(s + 1, (s + 1) & 1);
+    cpa_wait<1>();
+    __syncthreads();
+    const double* As = gsm + (s & 1) * (2 * BT * GSA);
+    const double* Bs = As + BT * GSA;
+    const int kq = min(GKS, L - s * GKS);  // valid K in this stage (zero-filled beyond)
+#pragma unroll 2
+    for (int q4 = 0; q4 < GKS; q4 += 4) {
+      if (q4 >= kq) break;
+      double a0[2], a1[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = 32 * wj + 16 * mt + g;
+        a0[mt] = As[row * GSA + q4 + t];
+        a1[mt] = As[(row + 8) * GSA + q4 + t];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int col = 16 * wk + 8 * nt + g;
+        const double b = Bs[col * GSA + q4 + t];
+        double bj = 0.0;
+        if (CPLX) {  // (J R): (b_im, -b_re) per complex entry
+          const double v = Bs[col * GSA + q4 + (t ^ 1)];
+          bj = (t & 1) ? -v : v;
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma(re[mt][nt], a0[mt], a1[mt], b);
+          if (CPLX) dmma(im[mt][nt], a0[mt], a1[mt], bj);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cpa_wait<0>();
+  // epilogue
+  double best = 0.0;
+  long long barg = LLONG_MAX;
+  double* G = P.ws.G + (long long)q.slot * P.ws.s_G;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = jb * BT + 32 * wj + 16 * mt + g + 8 * (e >> 1);
+        const int k = kb * BT + 16 * wk + 8 * nt + 2 * t + (e & 1);
+        if (j < k && k < N) {
+          const long long p = pair_index(j, k, N);
+          const double gr = re[mt][nt][e], gi = CPLX ? im[mt][nt][e] : 0.0;
+          if (MODE == 0) {
+            const double u = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+            const double xv = q.squared ? u : sqrt(u);
+            if (CPLX) {
+              *reinterpret_cast<double2*>(G + 2 * p) = make_double2(gr, gi);
+            } else {
+              G[p] = gr;
+            }
+            best = fmax(best, xv);
+          } else {
+            const double m = cas_hypot(gr, gi);  // std::abs = hypot (frame.hpp:87)
+            if (m > best || (m == best && m > 0.0 && p < barg)) {
+              best = m;
+              barg = p;
+            }
+          }
+        }
+      }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const double ov = __shfl_xor_sync(FULL, best, off);
+    const long long oi = __shfl_xor_sync(FULL, barg, off);
+    if (ov > best || (ov == best && oi < barg)) {
+      best = ov;
+      barg = oi;
+    }
+  }
+  if (lane == 0) {
+    red_v[warp] = best;
+    red_i[warp] = barg;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double v = red_v[0];
+    long long ix = red_i[0];
+    for (int w = 1; w < 8; ++w)
+      if (red_v[w] > v || (red_v[w] == v && red_i[w] < ix)) {
+        v = red_v[w];
+        ix = red_i[w];
+      }
+    if (MODE == 0) {
+      atomicMax(&P.outs[r].smax, (unsigned long long)__double_as_longlong(v));  // x >= 0: bits order like values
+    } else {
+      P.ws.tmu[(long long)q.slot * P.ws.s_tile + blockIdx.x] = v;
+      P.ws.targ[(long long)q.slot * P.ws.s_tile + blockIdx.x] = ix;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K3
+// w_p = exp((x_p - s)/delta), x_p recomputed from G exactly as K2 formed it;
+// the pairs of 16 consecutive rows (a contiguous range) summed over 256 CAS
+// lanes (lane l: pairs l, l+256, ... in order), xor butterfly, warp tree.
+template <bool CPLX>
+__global__ void __launch_bounds__(BZLANES) bde_weights(Pipe P) {
+  __shared__ double wt[BZLANES / 32];
+  const Shape& sh = P.sh;
+  const int r = P.active[blockIdx.y];
+  const Req q = P.reqs[r];
+  if (P.outs[r].zc != INT_MAX) return;
+  const double s = __longlong_as_double((long long)P.outs[r].smax);
+  const double cut = __dmul_rn(kUnderflowCut, q.delta);
+  const double yd = __drcp_rn(q.delta);
+  const bool chk = !(s >= 0x1.0p-800);  // else every nonzero |x - s| >= 2^-854 (Markstein exact)
+  const long long N = sh.N;
+  const long long r0 = (long long)blockIdx.x * BZROWS, r1 = min(N, r0 + BZROWS);
+  const long long p0 = r0 * N - r0 * (r0 + 1) / 2, p1 = r1 * N - r1 * (r1 + 1) / 2;
+  const double* G = P.ws.G + (long long)q.slot * P.ws.s_G;
+  double* W = P.ws.W + (long long)q.slot * P.ws.s_W;
+  double zp = 0.0;
+  for (long long p = p0 + threadIdx.x; p < p1; p += 4 * BZLANES) {
+    double xv[4], w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long pp = p + u * BZLANES;
+      double uu = 0.0;
+      if (pp < p1) {
+        if (CPLX) {
+          const double2 gg = *reinterpret_cast<const double2*>(G + 2 * pp);
+          uu = __dadd_rn(__dmul_rn(gg.x, gg.x), __dmul_rn(gg.y, gg.y));
+        } else {
+          const double gr = G[pp];
+          uu = __dmul_rn(gr, gr);
+        }
+      }
+      xv[u] = q.squared ? uu : sqrt(uu);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double diff = __dsub_rn(xv[u], s);
+      double y = div_fast(diff, q.delta, yd);
+      if (chk && diff < 0.0 && diff > -0x1.0p-900) y = __ddiv_rn(diff, q.delta);
+      const double e = cas_exp_core(y);  // the core domain wherever !(diff < cut)
+      w[u] = (diff < cut) ? 0.0 : e;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (p + u * BZLANES < p1) {
+        W[p + u * BZLANES] = w[u];
+        zp = __dadd_rn(zp, w[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) zp = __dadd_rn(zp, __shfl_xor_sync(FULL, zp, off));
+  if ((threadIdx.x & 31) == 0) wt[threadIdx.x >> 5] = zp;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < BZLANES / 32 ? wt[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int off = 1; off < BZLANES / 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+    if (threadIdx.x == 0) P.ws.zpart[(long long)q.slot * P.ws.s_zpart + blockIdx.x] = v;
+  }
+}
+
+// ---------------------------------------------------------------- K4
+__global__ void bde_zreduce(Pipe P) {
+  const int r = P.active[blockIdx.x];
+  const Req q = P.reqs[r];
+  if (threadIdx.x != 0) return;
+  ReqOut& o = P.outs[r];
+  if (o.zc != INT_MAX) {
+    o.F = __longlong_as_double(0x7ff0000000000000LL);
+    o.s = 0.0;
+    return;
+  }
+  const double* zp = P.ws.zpart + (long long)q.slot * P.ws.s_zpart;
+  const double s = __longlong_as_double((long long)o.smax);
+  double z = zp[0];
+  for (int b = 1; b < P.sh.nzb; ++b) z = __dadd_rn(z, zp[b]);
+  o.s = s;
+  o.z = z;
+  o.F = __dadd_rn(s, __dmul_rn(q.delta, cas_log(z)));
+}
+
+// ---------------------------------------------------------------- K5
+// D^T(m, i) = sum_k P(k, m) phi(i, k) over the k of chunk ch (ascending),
+// register-blocked on DMMA: rows m (64 per CTA), columns i (IB per CTA), 8
+// warps = 2 (m) x 4 (i).  Complex: one accumulator pair per (m, i); A = P^T
+// interleaved (pr, pi) per k, read as (pr, pi) for re and (pi, pr) for im;
+// B = phi interleaved, (fr, -fi) for re and (fr, fi) for im.  The P tile of a
+// stage is built from the packed (w, G) in registers one stage ahead (the
+// gather overlaps the MMAs) and stored to shared memory; the phi tile streams
+// in by cp.async.  i-block 0 also sums t_m = sum_k c u (ascending k, add).
+template <bool CPLX, int IB>
+struct GradCfg {
+  static constexpr int KK = CPLX ? 16 : 32;        // k per stage (interleaved K' = 32 either way)
+  static constexpr int KP = 32;                    // K' per stage
+  static constexpr int SA = KP + 4;                // P^T tile row stride (== 4 mod 16)
+  static constexpr int FW = CPLX ? 2 * IB : IB;    // doubles per phi row slice
+  static constexpr int SF = CPLX ? FW + 8 : FW + 4;  // == 8 / 4 mod 16: conflict-free fragments
+  static constexpr int NT = IB / 32;               // n8 tiles per warp (warp covers IB/4 columns)
+  static constexpr int A_D = BT * SA, F_D = KK * SF, CU_D = BT * KK;
+  static constexpr size_t smem = (size_t)(2 * A_D + 2 * F_D + CU_D) * sizeof(double);
+  static constexpr int EPT = BT * KK / 256;        // P elements gathered per thread per stage
+};
+
+template <bool CPLX, int IB>
+__global__ void __launch_bounds__(256, 1) bde_grad(Pipe P) {
+  using C = GradCfg<CPLX, IB>;
+  constexpr int KK = C::KK, SA = C::SA, SF = C::SF, FW = C::FW, NT = C::NT, EPT = C::EPT;
+  extern __shared__ __align__(16) double smem[];
+  double* Abuf = smem;                  // 2 x A_D
+  double* Fbuf = smem + 2 * C::A_D;     // 2 x F_D
+  double* CUs = Fbuf + 2 * C::F_D;      // CU_D
+  const Shape& sh = P.sh;
+  const int K = sh.K;
+  const int r = P.active[blockIdx.z / K], ch = blockIdx.z % K;
+  const Req q = P.reqs[r];
+  if (P.outs[r].zc != INT_MAX) return;
+  const int N = sh.N, L = sh.L, d = sh.d;
+  const int m0 = blockIdx.x * BT, i0 = blockIdx.y * IB;
+  const int k_lo = (int)(((long long)ch * N) / K), k_hi = (int)(((long long)(ch + 1) * N) / K);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wi = warp & 3;
+  const double* phi = P.ws.phi + (long long)q.slot * P.ws.s_phi;
+  const double* Gp = P.ws.G + (long long)q.slot * P.ws.s_G;
+  const double* Wp = P.ws.W + (long long)q.slot * P.ws.s_W;
+  const double z = P.outs[r].z;
+  const double yz = __drcp_rn(z);
+  const bool tsum = blockIdx.y == 0 && tid < BT;
+  double tacc = 0.0;
+
+  double re[2][NT][4], im[2][NT][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) re[a][b][e] = im[a][b][e] = 0.0;
+
+  // ---- P tile gather (registers), one stage ahead
+  double rw[EPT], rgr[EPT], rgi[EPT];
+  int rk[EPT], rm[EPT];
+  auto gather = [&](int k0) {
+    // rows of a stage tile above the diagonal read along m, below it along k (coalesced both ways)
+    const bool upper = k0 + KK <= m0;
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      const int e = tid + 256 * u;
+      const int mm = upper ? (e & (BT - 1)) : (e / KK);
+      const int kk = upper ? (e / BT) : (e % KK);
+      const int k = k0 + kk, m = m0 + mm;
+      rk[u] = kk;
+      rm[u] = mm;
+      rw[u] = 0.0;
+      rgr[u] = rgi[u] = 0.0;
+      if (k < k_hi && m < N && k != m) {
+        const long long p = k < m ? pair_index(k, m, N) : pair_index(m, k, N);
+        const double w = Wp[p];
+        rw[u] = w;
+        if (w != 0.0) {
+          if (CPLX) {
+            const double2 gg = *reinterpret_cast<const double2*>(Gp + 2 * p);
+            rgr[u] = gg.x;
+            rgi[u] = k < m ? gg.y : -gg.y;  // G(k, m) = conj(G(m, k)) below the diagonal
+          } else {
+            rgr[u] = Gp[p];
+          }
+        }
+      }
+    }
+  };
+  // coefficients c = w/z (Markstein == IEEE), P = c G, c u  -> shared memory
+  auto convert = [&](double* As) {
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+      double vr = 0.0, vi = 0.0, vu = 0.0;
+      if (rw[u] != 0.0) {
+        const double cq = div_rn(rw[u], z, yz);
+        if (cq != 0.0) {
+          const double gr = rgr[u], gi = rgi[u];
+          const double uu = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+          double cc = cq;
+          if (!q.squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(uu), 1e-150)));
+          vr = __dmul_rn(cc, gr);
+          vi = __dmul_rn(cc, gi);
+          vu = __dmul_rn(cc, uu);
+        }
+      }
+      const int mm = rm[u], kk = rk[u];
+      if (CPLX) {
+        As[mm * SA + 2 * kk] = vr;
+        As[mm * SA + 2 * kk + 1] = vi;
+      } else {
+        As[mm * SA + kk] = vr;
+      }
+      CUs[mm * KK + kk] = vu;
+    }
+  };
+  auto issue_phi = [&](int k0, double* Fs) {
+    // rows kk: phi column k0 + kk, components [i0 * (CPLX ? 2 : 1), + FW)
+    const int c0 = CPLX ? 2 * i0 : i0;
+    for (int e = tid; e < KK * FW; e += 256) {
+      const int kk = e / FW, c = e - kk * FW;
+      const int k = k0 + kk;
+      const bool v = k < k_hi && c0 + c < L;
+      cpa8(Fs + kk * SF + c, phi + (v ? (long long)k * L + c0 + c : 0), v);
+    }
+    cpa_commit();
+  };
+
+  const int nst = (k_hi - k_lo + KK - 1) / KK;
+  if (nst > 0) {
+    issue_phi(k_lo, Fbuf);
+    gather(k_lo);
+    convert(Abuf);
+    cpa_wait<0>();
+    __syncthreads();
+  }
+  for (int s = 0; s < nst; ++s) {
+    const int k0 = k_lo + s * KK;
+    const int cur = s & 1;
+    const bool more = s + 1 < nst;
+    if (more) {
+      issue_phi(k0 + KK, Fbuf + (cur ^ 1) * C::F_D);
+      gather(k0 + KK);
+    }
+    if (tsum) {  // t chunk partial: ascending k, plain adds (c u of this stage)
+      const int kmax = min(KK, k_hi - k0);
+      for (int kk = 0; kk < kmax; ++kk) tacc = __dadd_rn(tacc, CUs[tid * KK + kk]);
+    }
+    const double* As = Abuf + cur * C::A_D;
+    const double* Fs = Fbuf + cur * C::F_D;
+#pragma unroll 2
+    for (int q4 = 0; q4 < C::KP; q4 += 4) {
+      double ar0[2], ar1[2], ai0[2], ai1[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = 32 * wm + 16 * mt + g;
+        ar0[mt] = As[row * SA + q4 + t];
+        ar1[mt] = As[(row + 8) * SA + q4 + t];
+        if (CPLX) {
+          ai0[mt] = As[row * SA + q4 + (t ^ 1)];
+          ai1[mt] = As[(row + 8) * SA + q4 + (t ^ 1)];
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int col = (IB / 4) * wi + 8 * nt + g;  // i within the block
+        double br, bi = 0.0;
+        if (CPLX) {
+          const int qq = q4 + t;  // interleaved K': k = qq / 2, component qq & 1
+          const double v = Fs[(qq >> 1) * SF + 2 * col + (qq & 1)];
+          br = (qq & 1) ? -v : v;
+          bi = v;
+        } else {
+          br = Fs[(q4 + t) * SF + col];
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          dmma(re[mt][nt], ar0[mt], ar1[mt], br);
+          if (CPLX) dmma(im[mt][nt], ai0[mt], ai1[mt], bi);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with As[cur], Fs[cur] and CUs
+    if (more) {
+      convert(Abuf + (cur ^ 1) * C::A_D);
+      cpa_wait<0>();
+    }
+    __syncthreads();
+  }
+  // ---- outputs: chunk partials in the point layout
+  double* part = P.ws.part + (long long)q.slot * P.ws.s_part + (long long)ch * sh.dim;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + 32 * wm + 16 * mt + g + 8 * h;
+        const int i = i0 + (IB / 4) * wi + 8 * nt + 2 * t;
+        if (m >= N) continue;
+        if (CPLX) {
+          double* o = part + (long long)m * L + 2 * i;  // 16-byte aligned (L and 2i even)
+          if (i < d) *reinterpret_cast<double2*>(o) = make_double2(re[mt][nt][2 * h], im[mt][nt][2 * h]);
+          if (i + 1 < d) *reinterpret_cast<double2*>(o + 2) = make_double2(re[mt][nt][2 * h + 1], im[mt][nt][2 * h + 1]);
+        } else {
+          double* o = part + (long long)m * L + i;
+          if (i < d) o[0] = re[mt][nt][2 * h];
+          if (i + 1 < d) o[1] = re[mt][nt][2 * h + 1];
+        }
+      }
+  if (tsum && m0 + tid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + tid] = tacc;
+}
+
+// ---------------------------------------------------------------- K6
+__global__ void bde_finalize(Pipe P) {
+  const Shape& sh = P.sh;
+  const int r = P.active[blockIdx.y];
+  const Req q = P.reqs[r];
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= sh.dim) return;
+  if (P.outs[r].zc != INT_MAX) {
+    q.grad[e] = 0.0;
+    return;
+  }
+  const int m = (int)(e / sh.L);
+  const double* part = P.ws.part + (long long)q.slot * P.ws.s_part;
+  const double* tpart = P.ws.tpart + (long long)q.slot * P.ws.s_tpart;
+  double a = part[e], tt = tpart[m];
+  for (int ch = 1; ch < sh.K; ++ch) {
+    a = __dadd_rn(a, part[(long long)ch * sh.dim + e]);
+    tt = __dadd_rn(tt, tpart[(long long)ch * sh.N + m]);
+  }
+  const double ph = P.ws.phi[(long long)q.slot * P.ws.s_phi + e];
+  const double alpha = P.ws.alpha[(long long)q.slot * P.ws.s_alpha + m];
+  q.grad[e] = __dmul_rn(__ddiv_rn(__dsub_rn(a, __dmul_rn(tt, ph)), alpha), 2.0);
+}
+
+// softmax weights c_p = w_p / z (ObjectiveEval::softmax_weights), when asked
+__global__ void bde_wout(Pipe P) {
+  const int r = P.active[blockIdx.y];
+  const Req q = P.reqs[r];
+  if (!q.wout) return;
+  const long long n = P.sh.n;
+  const bool zc = P.outs[r].zc != INT_MAX;
+  const double z = P.outs[r].z, yz = __drcp_rn(z);
+  const double* W = P.ws.W + (long long)q.slot * P.ws.s_W;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const double w = zc ? 0.0 : W[p];
+    q.wout[p] = (w == 0.0) ? 0.0 : div_rn(w, z, yz);
+  }
+}
+
+// coherence: the tile maxima in (mu desc, pair asc) order
+__global__ void bde_coh_reduce(Pipe P) {
+  __shared__ double sv[256];
+  __shared__ long long si[256];
+  const int r = P.active[blockIdx.x];
+  const Req q = P.reqs[r];
+  ReqOut& o = P.outs[r];
+  const double* tm = P.ws.tmu + (long long)q.slot * P.ws.s_tile;
+  const long long* ta = P.ws.targ + (long long)q.slot * P.ws.s_tile;
+  double best = 0.0;
+  long long arg = LLONG_MAX;
+  for (int tt = threadIdx.x; tt < P.sh.tiles; tt += blockDim.x) {
+    const double v = tm[tt];
+    const long long a = ta[tt];
+    if (v > best || (v == best && v > 0.0 && a < arg)) {
+      best = v;
+      arg = a;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = arg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int u = 1; u < (int)blockDim.x; ++u)
+      if (sv[u] > best || (sv[u] == best && sv[u] > 0.0 && si[u] < arg)) {
+        best = sv[u];
+        arg = si[u];
+      }
+    const bool bad = q.kind == REQ_COH_NORM && o.zc != INT_MAX;
+    o.mu = bad ? 0.0 : best;
+    o.argmax = bad || arg == LLONG_MAX ? -1 : arg;
+  }
+}
+
+}  // namespace trstmi_bde

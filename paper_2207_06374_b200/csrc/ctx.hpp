@@ -8,6 +8,7 @@
 
 #include <string>
 
+#include "bde_engine.hpp"
 #include "large_engine.hpp"
 
 struct trstmi_ctx {
@@ -15,7 +16,8 @@ struct trstmi_ctx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   int* counter = nullptr;
-  trstmi_large::Engine* large = nullptr;  // large-frame path engine (lazy)
+  trstmi_large::Engine* large = nullptr;  // large-frame engine for the sharded single frame (lazy)
+  trstmi_bde_host::Engine* bde = nullptr; // batched large-frame engine (lazy)
   int large_workers = 8;                  // concurrent large-path trials (streams)
   int shard_world = 1;                    // single-frame row-block sharding (trstmi_set_shard)
   // multi-GPU trial scheduler (trstmi_comm_init): one process per GPU

@@ -191,7 +191,7 @@ extern "C" {
 
 int trstmi_version(void) { return 1; }
 
-long long trstmi_launch_count(void) { return g_launches + trstmi_large::launches(); }
+long long trstmi_launch_count(void) { return g_launches + trstmi_large::launches() + trstmi_bde_host::launches(); }
 
 // Measured FP64 FMA peak of the device (TFLOP/s, 2 flops per fma), timed with
 // CUDA events over `iters` x 128 fma per thread on a full-occupancy grid.
@@ -354,6 +354,7 @@ int trstmi_ctx_destroy(trstmi_ctx* ctx) {
   if (ctx->counter) cudaFree(ctx->counter);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->large) trstmi_large::engine_destroy(ctx->large);
+  if (ctx->bde) trstmi_bde_host::destroy(ctx->bde);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return TRSTMI_OK;
@@ -376,6 +377,11 @@ static trstmi_large::Engine* large_engine(trstmi_ctx* ctx, cudaStream_t st) {
   if (!ctx->large) ctx->large = trstmi_large::engine_create(ctx->device, st);
   trstmi_large::engine_set_stream(ctx->large, st);
   return ctx->large;
+}
+
+static trstmi_bde_host::Engine* bde_engine(trstmi_ctx* ctx) {
+  if (!ctx->bde) ctx->bde = trstmi_bde_host::create(ctx->device);
+  return ctx->bde;
 }
 
 // ------------------------------------------------------------------ eval / hvp / coherence
@@ -404,6 +410,22 @@ int trstmi_eval_batch_dev(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int6
   int rc = check_shape(ctx, field, d, N, "eval_objective");
   if (rc) return rc;
   cudaSetDevice(ctx->device);
+  if (trstmi_large::use_large(field, d, N) && ctx->shard_world == 1) {  // batched engine: all B points at once
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<double> hd(B), hF(B), hs(B);
+    std::vector<long long> hz(B);
+    CUDA_TRY(ctx, cudaMemcpyAsync(hd.data(), delta, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    const int r2 = trstmi_bde_host::eval_points(bde_engine(ctx), st, field, (int)d, (int)N, (int)B, pts, nullptr, nullptr,
+                                                hd.data(), squared, grad, weights, hF.data(), hs.data(), hz.data(),
+                                                &ctx->err);
+    if (r2) return r2;
+    CUDA_TRY(ctx, cudaMemcpyAsync(F, hF.data(), B * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(s, hs.data(), B * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(zero_col, hz.data(), B * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    return TRSTMI_OK;
+  }
   if (trstmi_large::use_large(field, d, N)) {
     const trstmi_large::Shape sh = trstmi_large::make_shape(field, (int)d, (int)N);
     cudaStream_t st = (cudaStream_t)stream;
@@ -495,6 +517,20 @@ int trstmi_hvp_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int64_t B
   CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, pts, vb, cudaMemcpyHostToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(dr.p, dirs, vb, cudaMemcpyHostToDevice, st));
   CUDA_TRY(ctx, cudaMemcpyAsync(dd.p, delta, B * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (trstmi_large::use_large(field, d, N) && ctx->shard_world == 1) {
+    std::vector<int> hp(B);
+    std::vector<long long> hz(B);
+    const int r2 = trstmi_bde_host::hvp_points(bde_engine(ctx), st, field, (int)d, (int)N, (int)B, (double*)dp.p,
+                                               (double*)dr.p, delta, (double*)dh.p, hp.data(), hz.data(), &ctx->err);
+    if (r2) return r2;
+    for (int64_t b = 0; b < B; ++b) {
+      path[b] = hp[b];
+      zero_col[b] = hz[b];
+    }
+    CUDA_TRY(ctx, cudaMemcpyAsync(hv, dh.p, vb, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+    return TRSTMI_OK;
+  }
   if (trstmi_large::use_large(field, d, N)) {
     const trstmi_large::Shape sh = trstmi_large::make_shape(field, (int)d, (int)N);
     trstmi_large::Engine* E = large_engine(ctx, st);
@@ -545,6 +581,17 @@ int trstmi_coherence_batch(trstmi_ctx* ctx, int field, int64_t d, int64_t N, int
   CUDA_TRY(ctx, cudaMalloc(&dz.p, B * sizeof(int64_t)));
   cudaStream_t st = ctx->stream;
   CUDA_TRY(ctx, cudaMemcpyAsync(dp.p, frames, vb, cudaMemcpyHostToDevice, st));
+  if (trstmi_large::use_large(field, d, N) && ctx->shard_world == 1) {
+    std::vector<long long> ha(B), hz(B);
+    const int r2 = trstmi_bde_host::coherence_points(bde_engine(ctx), st, field, (int)d, (int)N, (int)B, (double*)dp.p,
+                                                     normalize, mu, ha.data(), hz.data(), &ctx->err);
+    if (r2) return r2;
+    for (int64_t b = 0; b < B; ++b) {
+      argmax_pair[b] = ha[b];
+      zero_col[b] = hz[b];
+    }
+    return TRSTMI_OK;
+  }
   if (trstmi_large::use_large(field, d, N)) {
     const trstmi_large::Shape sh = trstmi_large::make_shape(field, (int)d, (int)N);
     trstmi_large::Engine* E = large_engine(ctx, st);
@@ -650,6 +697,19 @@ int trstmi_solve_batch_dev(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t trial
   if (rc) return rc;
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
+  if (trstmi_large::use_large(cfg->field, cfg->d, cfg->N) && ctx->shard_world == 1) {
+    // batched engine: every trial's trust-region state machine on the device, one
+    // launch per pipeline kernel per tick for all trials in flight
+    const trstmi_bde_host::TrCfg tr{A.tr.delta0, A.tr.delta_max, A.tr.eta,      A.tr.shrink, A.tr.grow,
+                                    A.tr.grad_tol, A.tr.cg_force_c, A.tr.max_outer, A.tr.max_cg};
+    const int cap = A.record_cap;
+    if (stage_out_dev)
+      CUDA_TRY(ctx, cudaMemsetAsync(stage_out_dev, 0, (size_t)trials * A.n_stages * sizeof(trstmi_stage_out), st));
+    if (outer_out_dev && cap)
+      CUDA_TRY(ctx, cudaMemsetAsync(outer_out_dev, 0, (size_t)trials * cap * sizeof(trstmi_outer_out), st));
+    return trstmi_bde_host::anneal(bde_engine(ctx), st, cfg->field, cfg->d, cfg->N, tr, sched, cap, trials, params_dev,
+                                   frames_dev, rng_state, trial_out_dev, stage_out_dev, outer_out_dev, &ctx->err);
+  }
   if (trstmi_large::use_large(cfg->field, cfg->d, cfg->N)) {
     const trstmi_large::Shape sh = trstmi_large::make_shape(cfg->field, cfg->d, cfg->N);
     trstmi_large::TrCfg tr{A.tr.delta0, A.tr.delta_max, A.tr.eta, A.tr.shrink, A.tr.grow, A.tr.grad_tol,
