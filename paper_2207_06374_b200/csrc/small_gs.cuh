@@ -27,7 +27,13 @@
 #pragma once
 #include "small_path.cuh"
 
+#ifndef TRSTMI_GS_UNROLL
+#define TRSTMI_GS_UNROLL 4
+#endif
+
 namespace trstmi_dev {
+
+constexpr int kGsUnroll = TRSTMI_GS_UNROLL;  // k steps of the branch-free gradient loop in flight
 
 // Slot tables and zeroed pair arrays.  Once per kernel; ends with a barrier.
 template <int S, bool CPLX>
@@ -266,7 +272,7 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
 #pragma unroll
     for (int q = 0; q < LM; ++q) acc[q] = 0.0;
     double tp = 0.0;
-    auto term = [&](int k, int slot, bool lower) {
+    auto term = [&](int k, int slot, bool lower, auto chk_tag) {
       const double w = U[slot];
       double re, im = 0.0;
       if constexpr (CPLX) {
@@ -277,7 +283,8 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
         re = GRI[slot];
       }
       double c = div_fast(w, z, yz);
-      if (chkdiv && w > 0.0 && w < 0x1.0p-900) c = ieee_div(w, z);
+      if constexpr (decltype(chk_tag)::value)  // some w may be < 2^-900: its Markstein quotient is not exact
+        if (w > 0.0 && w < 0x1.0p-900) c = ieee_div(w, z);
       const double uu = CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re);
       if constexpr (!SQ) c = __dmul_rn(c, __ddiv_rn(0.5, fmax(sqrt(uu), 1e-150)));
       tp = __dadd_rn(tp, __dmul_rn(c, uu));
@@ -314,14 +321,20 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
           const int k = base + __ffs(wd) - 1;
           wd &= wd - 1;
           const bool lower = k < m;
-          term(k, lower ? fk[k] + m : fm + k, lower);
+          term(k, lower ? fk[k] + m : fm + k, lower, BoolTag<true>{});
         }
       }
-    } else {
+    } else if (chkdiv) {
 #pragma unroll 2
       for (int k = k_lo; k < k_hi; ++k) {
         const bool lower = k < m;
-        term(k, lower ? fk[k] + m : fm + k, lower);
+        term(k, lower ? fk[k] + m : fm + k, lower, BoolTag<true>{});
+      }
+    } else {  // the common case, branch-free: consecutive k steps interleave
+#pragma unroll kGsUnroll
+      for (int k = k_lo; k < k_hi; ++k) {
+        const bool lower = k < m;
+        term(k, lower ? fk[k] + m : fm + k, lower, BoolTag<false>{});
       }
     }
     double* pp = sm.part + (long long)unit * (L + 1);

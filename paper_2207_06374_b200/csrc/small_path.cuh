@@ -149,13 +149,16 @@ __device__ __forceinline__ double block_sum1(double v, double* red, int& rbuf) {
   return a[0];
 }
 
-template <int S>
+// WS: warps the scratch buffers are strided for (the CAS lane count / 32 when
+// the CTA has fewer threads than CAS lanes, small_rt.cuh) — every reduction
+// of a kernel must use the same stride, or the two alternating buffers overlap.
+template <int S, int WS = S / 32>
 __device__ __forceinline__ double block_max(double v, double* red, int& rbuf) {
   constexpr int W = S / 32;
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
   if constexpr (W > 1) {
-    double* buf = red + rbuf * (4 * W);
+    double* buf = red + rbuf * (4 * WS);
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -190,7 +193,7 @@ __device__ __forceinline__ int block_min_int(int v, int* ired, int& ibuf) {
 
 // (value, index) max with the lowest index on ties: the first strict maximum
 // in pair order (frame.hpp:141-143).
-template <int S>
+template <int S, int WS = S / 32>
 __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* red, int& rbuf) {
   constexpr int W = S / 32;
 #pragma unroll
@@ -203,7 +206,7 @@ __device__ __forceinline__ void block_argmax(double& v, long long& idx, double* 
     }
   }
   if constexpr (W > 1) {
-    double* buf = red + rbuf * (4 * W);
+    double* buf = red + rbuf * (4 * WS);
     if ((threadIdx.x & 31) == 0) {
       buf[threadIdx.x >> 5] = v;
       buf[W + (threadIdx.x >> 5)] = __longlong_as_double(idx);

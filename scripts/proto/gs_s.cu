@@ -1,0 +1,51 @@
+// GS eval throughput at a given S (threads = CAS lanes), one CTA per SM.
+#include "batch_kernels.cuh"
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+using namespace trstmi_dev;
+#ifndef NVEC
+#define NVEC 3
+#endif
+#ifndef SS
+#define SS 1024
+#endif
+template <bool CPLX, int DMAX, bool EXACT, int S, bool GS>
+__global__ void __launch_bounds__(S, 1) eval_k(const BatchArgs A) {
+  extern __shared__ __align__(16) double smem_raw[];
+  Smem sm;
+  double* v[3];
+  carve<CPLX>(A.P, S, smem_raw, sm, v, 3);
+  build_tables<S, CPLX, GS>(A.P, sm);
+  int rbuf = 0;
+  for (long long b = blockIdx.x; b < A.B; b += gridDim.x) {
+    const double* x = A.pts + b * A.P.dim;
+    const int zc = eval_any<CPLX, DMAX, EXACT, S, GS, true>(A.P, x, nullptr, 0.0, A.delta[b], sm, rbuf, A.out + b * A.P.dim, &sm.scal[0], &sm.scal[1], nullptr);
+    if (threadIdx.x == 0) { A.F[b] = sm.scal[0]; A.s[b] = sm.scal[1]; A.zero_col[b] = zc; }
+    __syncthreads();
+  }
+}
+int main(int argc, char** argv) {
+  const int N = atoi(argv[1]); const double delta = atof(argv[2]);
+  const int B = 148 * 8, d = 2;
+  Prob P = make_small_prob(true, d, N, kchunks_for(d, N, SS), 1, 1);
+  std::vector<double> h((size_t)B * P.dim); srand(1); for (auto& v : h) v = rand() / (double)RAND_MAX - 0.5;
+  double *x, *dl, *F, *s, *g; long long* zc;
+  cudaMalloc(&x, h.size() * 8); cudaMemcpy(x, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  std::vector<double> hd(B, delta); cudaMalloc(&dl, B * 8); cudaMemcpy(dl, hd.data(), B * 8, cudaMemcpyHostToDevice);
+  cudaMalloc(&F, B * 8); cudaMalloc(&s, B * 8); cudaMalloc(&g, h.size() * 8); cudaMalloc(&zc, B * 8);
+  BatchArgs A{}; A.P = P; A.B = B; A.pts = x; A.delta = dl; A.squared = 1; A.F = F; A.s = s; A.out = g; A.zero_col = zc;
+  const void* fn = (const void*)&eval_k<true, 2, true, SS, true>;
+  const size_t bytes = smem_doubles(P, SS, true, NVEC) * 8;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  void* args[] = {&A};
+  cudaLaunchKernel(fn, dim3(148), dim3(SS), args, bytes, 0);
+  cudaError_t e2 = cudaDeviceSynchronize();
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
+  cudaEventRecord(e0);
+  for (int r = 0; r < 20; ++r) cudaLaunchKernel(fn, dim3(148), dim3(SS), args, bytes, 0);
+  cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+  const double ev = (double)B * 20 / (ms * 1e-3);
+  double F0; cudaMemcpy(&F0, F, 8, cudaMemcpyDeviceToHost);
+  printf("gs S=%d K=%d smem %zu (%s / %s): %.4g evals/s, %.0f SM-cycles/eval, F[0]=%.17g\n", SS, P.K, bytes, cudaGetErrorString(e), cudaGetErrorString(e2), ev, 148 * 1.965e9 / ev, F0);
+}
