@@ -652,6 +652,286 @@ __global__ void __launch_bounds__(256, 1) bde_grad(Pipe P) {
   if (tsum && m0 + tid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + tid] = tacc;
 }
 
+// ---------------------------------------------------------------- K5 (warp-specialised)
+// The same contraction as bde_grad with the work split by warp role, so the
+// tensor pipe never waits for the coefficient tiles:
+//   * producer warps gather the packed (w, G) of a stage from HBM / L2, form
+//     c = w/z, P = c G (conjugated below the diagonal) and c u, store the P^T
+//     tile, and stream the phi tile in by 16-byte cp.async one stage ahead;
+//     they also carry the t chunk partials sum_k c u (ascending k, plain adds);
+//   * consumer warps (WM (m) x WI (i)) run the DMMA loop; accumulators are
+//     MT x NT m16n8 tiles per warp (complex d = 128: 16 warps of 16 x 32, 64
+//     accumulator registers each, four warps per scheduler).
+// NST stage buffers cycle through named barriers (full[b]: producers arrive,
+// consumers sync; empty[b]: consumers arrive, producers sync).  A CTA walks
+// CPG consecutive CAS chunks of k (grid.z = requests x chunk groups): at a
+// chunk end the consumers store that chunk's partial and restart from +0 —
+// per output the ascending-k fma chain of its chunk, as before.
+template <bool CPLX, int IB>
+struct GradWsCfg {
+  static constexpr int KK = CPLX ? 16 : 32;
+  static constexpr int KP = 32;
+  static constexpr int SA = KP + 4;
+  static constexpr int FW = CPLX ? 2 * IB : IB;
+  static constexpr int SF = CPLX ? FW + 8 : FW + 4;
+  static constexpr int WI = 4;                                 // consumer warps along i
+  static constexpr int WM = (CPLX && IB >= 128) ? 4 : 2;       // ... along m
+  static constexpr int MT = BT / (16 * WM), NT = IB / (8 * WI);
+  static constexpr int A_D = BT * SA, F_D = KK * SF, CU_D = BT * KK;
+  static constexpr int NST = 3;
+  static constexpr int NPROD = CPLX ? 128 : 256;  // real stages hold twice the k
+  static constexpr int NCONS = 32 * WM * WI, NTHR = NPROD + NCONS;
+  static constexpr size_t smem = (size_t)(NST * (A_D + F_D) + 2 * CU_D) * sizeof(double);
+  static constexpr int EPT = BT * KK / NPROD;
+};
+
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+template <bool CPLX, int IB>
+__global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe P, int KS) {
+  using C = GradWsCfg<CPLX, IB>;
+  constexpr int KK = C::KK, SA = C::SA, SF = C::SF, FW = C::FW, MT = C::MT, NT = C::NT, EPT = C::EPT, NST = C::NST;
+  constexpr int NPROD = C::NPROD, NTHR = C::NTHR, WM = C::WM, WI = C::WI;
+  constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + NST, BAR_PROD = 1 + 2 * NST;
+  extern __shared__ __align__(16) double smem[];
+  double* Abuf = smem;                       // NST x A_D
+  double* Fbuf = smem + NST * C::A_D;        // NST x F_D
+  double* CUbuf = Fbuf + NST * C::F_D;       // 2 x CU_D
+  const Shape& sh = P.sh;
+  const int K = sh.K;
+  const int r = P.active[blockIdx.z / KS], cg = blockIdx.z % KS;
+  const Req q = P.reqs[r];
+  if (P.outs[r].zc != INT_MAX) return;
+  const int N = sh.N, L = sh.L, d = sh.d;
+  const int m0 = blockIdx.x * BT, i0 = blockIdx.y * IB;
+  const int CPG = (K + KS - 1) / KS;
+  const int ch_lo = cg * CPG, ch_hi = min(K, ch_lo + CPG);
+  if (ch_lo >= ch_hi) return;
+  const int tid = threadIdx.x;
+  const double* phi = P.ws.phi + (long long)q.slot * P.ws.s_phi;
+  auto chunk_lo = [&](int ch) { return (int)(((long long)ch * N) / K); };
+
+  if (tid < NPROD) {
+    // ======================================================= producers
+    const double* Gp = P.ws.G + (long long)q.slot * P.ws.s_G;
+    const double* Wp = P.ws.W + (long long)q.slot * P.ws.s_W;
+    const double z = P.outs[r].z;
+    const double yz = __drcp_rn(z);
+    const bool tsum = blockIdx.y == 0 && tid < BT;
+    double rw[EPT], rgr[EPT], rgi[EPT];  // the packed (w, G) of the stage to convert next
+    auto elem = [&](int k0, int u, int& mm, int& kk) {
+      // rows of a stage tile above the diagonal read along m, else along k (coalesced both ways)
+      const bool upper = k0 + KK <= m0;
+      const int e = tid + NPROD * u;
+      mm = upper ? (e & (BT - 1)) : (e / KK);
+      kk = upper ? (e / BT) : (e % KK);
+    };
+    auto gather = [&](int k0, int k_hi) {
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) {
+        int mm, kk;
+        elem(k0, u, mm, kk);
+        const int k = k0 + kk, m = m0 + mm;
+        double w = 0.0, gr = 0.0, gi = 0.0;
+        if (k < k_hi && m < N && k != m) {
+          const int lo = min(k, m), hi = max(k, m);
+          const int p = lo * N - ((lo * (lo + 1)) >> 1) + (hi - lo - 1);  // pair index: 32 bits up to N = 16384
+          w = Wp[p];
+          if (CPLX) {  // raw loads only: nothing here waits for the data (the conjugation is applied in convert)
+            const double2 gg = *reinterpret_cast<const double2*>(Gp + 2 * p);
+            gr = gg.x;
+            gi = gg.y;
+          } else {
+            gr = Gp[p];
+          }
+        }
+        rw[u] = w;
+        rgr[u] = gr;
+        rgi[u] = gi;
+      }
+    };
+    auto convert = [&](int k0, double* As, double* CUs) {
+#pragma unroll
+      for (int u = 0; u < EPT; ++u) {
+        int mm, kk;
+        elem(k0, u, mm, kk);
+        double vr = 0.0, vi = 0.0, vu = 0.0;
+        const double w = rw[u];
+        if (w != 0.0) {
+          const double cq = div_rn(w, z, yz);
+          if (cq != 0.0) {
+            // G(k, m) = conj(G(m, k)) below the diagonal (k > m: the packed entry is G(m, k))
+            const double gr = rgr[u], gi = (k0 + kk < m0 + mm) ? rgi[u] : -rgi[u];
+            const double uu = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
+            double cc = cq;
+            if (!q.squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(uu), 1e-150)));
+            vr = __dmul_rn(cc, gr);
+            vi = __dmul_rn(cc, gi);
+            vu = __dmul_rn(cc, uu);
+          }
+        }
+        if (CPLX) {
+          *reinterpret_cast<double2*>(As + mm * SA + 2 * kk) = make_double2(vr, vi);
+        } else {
+          As[mm * SA + kk] = vr;
+        }
+        CUs[mm * KK + kk] = vu;
+      }
+    };
+    auto issue_phi = [&](int k0, int k_hi, double* Fs) {
+      // rows kk: phi column k0 + kk, components [c0, c0 + FW); 16-byte copies (complex: c0, FW, SF, L all even;
+      // a real frame with odd d copies 8 bytes at a time)
+      const int c0 = CPLX ? 2 * i0 : i0;
+      if (CPLX || (L % 2 == 0)) {
+        for (int e = tid; e < KK * (FW / 2); e += NPROD) {
+          const int kk = e / (FW / 2), c = 2 * (e - kk * (FW / 2));
+          const int k = k0 + kk;
+          const bool v = k < k_hi && c0 + c < L;
+          cpa16(Fs + kk * SF + c, phi + (v ? (long long)k * L + c0 + c : 0), v);
+        }
+      } else {
+        for (int e = tid; e < KK * FW; e += NPROD) {
+          const int kk = e / FW, c = e - kk * FW;
+          const int k = k0 + kk;
+          const bool v = k < k_hi && c0 + c < L;
+          cpa8(Fs + kk * SF + c, phi + (v ? (long long)k * L + c0 + c : 0), v);
+        }
+      }
+    };
+    // stage (ch, s) -> the next stage, across chunk ends
+    auto next_stage = [&](int ch, int s, int& ch2, int& s2) {
+      const int nst = (chunk_lo(ch + 1) - chunk_lo(ch) + KK - 1) / KK;
+      ch2 = ch;
+      s2 = s + 1;
+      if (s2 >= nst) {
+        ch2 = ch + 1;
+        s2 = 0;
+      }
+      return ch2 < ch_hi;
+    };
+    int gs = 0;  // global stage counter (buffer cycling)
+    // prologue: the first stage's phi tile and packed (w, G) in flight
+    issue_phi(chunk_lo(ch_lo), chunk_lo(ch_lo + 1), Fbuf);
+    cpa_commit();
+    gather(chunk_lo(ch_lo), chunk_lo(ch_lo + 1));
+    for (int ch = ch_lo; ch < ch_hi; ++ch) {
+      const int k_lo = chunk_lo(ch), k_hi = chunk_lo(ch + 1);
+      const int nst = (k_hi - k_lo + KK - 1) / KK;
+      double tacc = 0.0;
+      for (int s = 0; s < nst; ++s, ++gs) {
+        const int k0 = k_lo + s * KK;
+        const int b = gs % NST;
+        int ch2, s2;
+        const bool more = next_stage(ch, s, ch2, s2);
+        const int b2 = (gs + 1) % NST;
+        // the next stage's phi tile streams in while this stage is converted
+        if (more) {
+          if (gs + 1 >= NST) nbar_sync(BAR_EMPTY + b2, NTHR);  // consumers are done with buffer b2
+          issue_phi(chunk_lo(ch2) + s2 * KK, chunk_lo(ch2 + 1), Fbuf + b2 * C::F_D);
+        }
+        cpa_commit();
+        double* CUs = CUbuf + (gs & 1) * C::CU_D;
+        convert(k0, Abuf + b * C::A_D, CUs);
+        cpa_wait<1>();  // this stage's phi tile (committed one iteration ago) has landed
+        __threadfence_block();
+        nbar_arrive(BAR_FULL + b, NTHR);
+        if (more) gather(chunk_lo(ch2) + s2 * KK, chunk_lo(ch2 + 1));  // lands during the consumers' stage
+        nbar_sync(BAR_PROD, NPROD);  // CUs complete (and the previous stage's t sums read)
+        if (tsum) {  // t chunk partial: ascending k, plain adds (c u of this stage)
+          const int kmax = min(KK, k_hi - k0);
+          for (int kk = 0; kk < kmax; ++kk) tacc = __dadd_rn(tacc, CUs[tid * KK + kk]);
+        }
+      }
+      if (tsum && m0 + tid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + tid] = tacc;
+    }
+    cpa_wait<0>();
+  } else {
+    // ======================================================= consumers
+    const int ctid = tid - NPROD, lane = ctid & 31, warp = ctid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp / WI, wi = warp % WI;
+    const int rbase = (BT / WM) * wm, cbase = (IB / WI) * wi;
+    double re[MT][NT][4], im[MT][NT][4];
+    int gs = 0;
+    for (int ch = ch_lo; ch < ch_hi; ++ch) {
+      const int k_lo = chunk_lo(ch), k_hi = chunk_lo(ch + 1);
+      const int nst = (k_hi - k_lo + KK - 1) / KK;
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b2 = 0; b2 < NT; ++b2)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) re[a][b2][e] = im[a][b2][e] = 0.0;
+      for (int s = 0; s < nst; ++s, ++gs) {
+        const int b = gs % NST;
+        nbar_sync(BAR_FULL + b, NTHR);
+        const double* As = Abuf + b * C::A_D;
+        const double* Fs = Fbuf + b * C::F_D;
+#pragma unroll 2
+        for (int q4 = 0; q4 < C::KP; q4 += 4) {
+          double ar0[MT], ar1[MT], ai0[MT], ai1[MT];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const int row = rbase + 16 * mt + g;
+            ar0[mt] = As[row * SA + q4 + t];
+            ar1[mt] = As[(row + 8) * SA + q4 + t];
+            if (CPLX) {
+              ai0[mt] = As[row * SA + q4 + (t ^ 1)];
+              ai1[mt] = As[(row + 8) * SA + q4 + (t ^ 1)];
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int col = cbase + 8 * nt + g;  // i within the block
+            double br, bi = 0.0;
+            if (CPLX) {
+              const int qq = q4 + t;  // interleaved K': k = qq / 2, component qq & 1
+              const double v = Fs[(qq >> 1) * SF + 2 * col + (qq & 1)];
+              br = (qq & 1) ? -v : v;
+              bi = v;
+            } else {
+              br = Fs[(q4 + t) * SF + col];
+            }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              dmma(re[mt][nt], ar0[mt], ar1[mt], br);
+              if (CPLX) dmma(im[mt][nt], ai0[mt], ai1[mt], bi);
+            }
+          }
+        }
+        nbar_arrive(BAR_EMPTY + b, NTHR);
+      }
+      // ---- this chunk's partial, point layout
+      double* part = P.ws.part + (long long)q.slot * P.ws.s_part + (long long)ch * sh.dim;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = m0 + rbase + 16 * mt + g + 8 * h;
+            const int i = i0 + cbase + 8 * nt + 2 * t;
+            if (m >= N) continue;
+            if (CPLX) {
+              double* o = part + (long long)m * L + 2 * i;  // 16-byte aligned (L and 2i even)
+              if (i < d) *reinterpret_cast<double2*>(o) = make_double2(re[mt][nt][2 * h], im[mt][nt][2 * h]);
+              if (i + 1 < d)
+                *reinterpret_cast<double2*>(o + 2) = make_double2(re[mt][nt][2 * h + 1], im[mt][nt][2 * h + 1]);
+            } else {
+              double* o = part + (long long)m * L + i;
+              if (i < d) o[0] = re[mt][nt][2 * h];
+              if (i + 1 < d) o[1] = re[mt][nt][2 * h + 1];
+            }
+          }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K6
 __global__ void bde_finalize(Pipe P) {
   const Shape& sh = P.sh;

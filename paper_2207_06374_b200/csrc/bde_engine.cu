@@ -237,13 +237,31 @@ static int ib_for(const Shape& sh) {
   return sh.d > 32 ? 64 : 32;
 }
 
+// Chunk groups per request: a CTA walks K / KS consecutive CAS chunks (one software pipeline over all of
+// them); the k range is split only as far as the grid needs to fill the GPU (~3 CTAs per SM).
+static int chunk_groups(const Shape& sh, int ib, int nreq) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long per = (long long)((sh.N + BT - 1) / BT) * ((sh.d + ib - 1) / ib) * nreq;
+  long long ks = (3LL * sms + per - 1) / per;
+  if (ks < 1) ks = 1;
+  if (ks > sh.K) ks = sh.K;
+  return (int)ks;
+}
+
 template <bool CPLX, int IB>
 static cudaError_t launch_grad(const Pipe& P, int nreq, cudaStream_t st) {
-  using C = GradCfg<CPLX, IB>;
-  const cudaError_t e = ensure_smem((const void*)bde_grad<CPLX, IB>, C::smem);
+  using C = GradWsCfg<CPLX, IB>;
+  const cudaError_t e = ensure_smem((const void*)bde_grad_ws<CPLX, IB>, C::smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((P.sh.N + BT - 1) / BT, (P.sh.d + IB - 1) / IB, P.sh.K * nreq);
-  bde_grad<CPLX, IB><<<grid, 256, C::smem, st>>>(P);
+  const int KS = chunk_groups(P.sh, IB, nreq);
+  dim3 grid((P.sh.N + BT - 1) / BT, (P.sh.d + IB - 1) / IB, KS * nreq);
+  bde_grad_ws<CPLX, IB><<<grid, C::NTHR, C::smem, st>>>(P, KS);
   return cudaGetLastError();
 }
 

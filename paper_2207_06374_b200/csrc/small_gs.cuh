@@ -25,6 +25,8 @@
 // Reference: eval_objective, smoothing.hpp:82-162 (paths under
 // /root/reference/proj/include/trstmi).
 #pragma once
+#include <type_traits>
+
 #include "small_path.cuh"
 
 #ifndef TRSTMI_GS_UNROLL
@@ -198,46 +200,68 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
   const bool chk = !(s >= 0x1.0p-800);
   double zl = 0.0;
   int nnz = 0, tiny = 0;
-  // two pairs (p, p + S) per step inside ONE conditional region, so their
-  // exp chains interleave (a branch per pair serialises them)
-  for (int p = tid; p < n; p += 2 * S) {
-    const int p2 = p + S;
-    const bool v2 = p2 < n;
-    const unsigned t1 = tab[p], t2 = tab[v2 ? p2 : p];
-    const int ph1 = (int)(t1 & 0xffffu), ph2 = (int)(t2 & 0xffffu);
-    const double d1 = __dsub_rn(U[ph1], s), d2 = __dsub_rn(U[ph2], s);
-    const bool k1 = !(d1 < cut), k2 = v2 && !(d2 < cut);  // NaN propagates like cas_exp
-    double w1 = 0.0, w2 = 0.0;
-    if (k1 | k2) {
-      double y1 = div_fast(d1, delta, ydelta), y2 = div_fast(d2, delta, ydelta);
-      if (chk) {
-        if (d1 < 0.0 && d1 > -0x1.0p-900) y1 = ieee_div(d1, delta);
-        if (d2 < 0.0 && d2 > -0x1.0p-900) y2 = ieee_div(d2, delta);
+  // UW pairs (p, p + S, ...) per step inside ONE conditional region, so their
+  // exp chains interleave (a branch per pair serialises them); z accumulates in
+  // the CAS lane order p, p + S, ...
+  auto exp_sweep = [&](auto uw_tag) {
+    constexpr int UW = decltype(uw_tag)::value;
+    for (int p0 = tid; p0 < n; p0 += UW * S) {
+      unsigned t[UW];
+      int ph[UW];
+      double dd[UW], w[UW];
+      bool kk[UW];
+      bool any = false;
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        const int p = p0 + u * S;
+        t[u] = tab[p < n ? p : p0];
+        ph[u] = (int)(t[u] & 0xffffu);
+        dd[u] = __dsub_rn(U[ph[u]], s);
+        kk[u] = p < n && !(dd[u] < cut);  // NaN propagates like cas_exp
+        any |= kk[u];
+        w[u] = 0.0;
       }
-      const double e1 = TRSTMI_EXP_CORE(y1), e2 = TRSTMI_EXP_CORE(y2);  // |y| <= 746 (+1 ulp) where taken
-      w1 = k1 ? e1 : 0.0;
-      w2 = k2 ? e2 : 0.0;
-      nnz += (int)k1 + (int)k2;                           // upper bound: only picks the gradient loop
-      tiny |= (k1 && y1 < -620.0) | (k2 && y2 < -620.0);  // w may be < 2^-900: phase 4 checks its quotients
-      if (build_mask) {
-        if (k1) {
-          const int j = (int)((t1 >> 16) & 0xffu), k = (int)(t1 >> 24);
-          atomicOr(&sm.mask[j * NW + (k >> 5)], 1u << (k & 31));
-          atomicOr(&sm.mask[k * NW + (j >> 5)], 1u << (j & 31));
+      if (any) {
+        double y[UW];
+#pragma unroll
+        for (int u = 0; u < UW; ++u) y[u] = div_fast(dd[u], delta, ydelta);
+        if (chk) {
+#pragma unroll
+          for (int u = 0; u < UW; ++u)
+            if (dd[u] < 0.0 && dd[u] > -0x1.0p-900) y[u] = ieee_div(dd[u], delta);
         }
-        if (k2) {
-          const int j = (int)((t2 >> 16) & 0xffu), k = (int)(t2 >> 24);
-          atomicOr(&sm.mask[j * NW + (k >> 5)], 1u << (k & 31));
-          atomicOr(&sm.mask[k * NW + (j >> 5)], 1u << (j & 31));
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          const double e = TRSTMI_EXP_CORE(y[u]);  // |y| <= 746 (+1 ulp) where taken
+          w[u] = kk[u] ? e : 0.0;
+          nnz += (int)kk[u];                        // upper bound: only picks the gradient loop
+          tiny |= (int)(kk[u] && y[u] < -620.0);    // w may be < 2^-900: phase 4 checks its quotients
+        }
+        if (build_mask) {
+#pragma unroll
+          for (int u = 0; u < UW; ++u) {
+            if (kk[u]) {
+              const int j = (int)((t[u] >> 16) & 0xffu), k = (int)(t[u] >> 24);
+              atomicOr(&sm.mask[j * NW + (k >> 5)], 1u << (k & 31));
+              atomicOr(&sm.mask[k * NW + (j >> 5)], 1u << (j & 31));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        if (p0 + u * S < n) {
+          U[ph[u]] = w[u];
+          zl = __dadd_rn(zl, w[u]);
         }
       }
     }
-    U[ph1] = w1;
-    zl = __dadd_rn(zl, w1);  // CAS lane order: p, then p + S
-    if (v2) {
-      U[ph2] = w2;
-      zl = __dadd_rn(zl, w2);
-    }
+  };
+  {
+    // five pairs per step where a thread owns several (config 2: 9.7, config 3: 4.9); the 64-lane layout of
+    // tiny frames (a pair or two per thread) keeps two.  One width per kernel: a run-time choice of widths
+    // triples the sweep's code and slowed every phase by 15 % (profiles/r2_c2_occupancy_experiments.md)
+    exp_sweep(std::integral_constant<int, (S <= 64 ? 2 : 5)>{});
   }
   double zz[3] = {zl, (double)nnz, (double)tiny};
   block_sum<S, 3>(zz, sm.red, rbuf);

@@ -82,31 +82,32 @@ __device__ __forceinline__ double block_dot(const double* a, const double* b, in
 }
 
 // ------------------------------------------------------------------ tiled pair sweep
-// Every pair (j, k), j < k, exactly once: warps take blocks of four rows of a
-// 32-column segment (segments anchored at the right edge, k = khi - 32 + lane),
-// round-robin over all blocks of all segments.  f(j[4], rowvalid[4], k, pk) —
+// Every pair (j, k), j < k, exactly once: a warp owns 32 consecutive columns k
+// (one per lane, in registers; segments anchored at the right edge,
+// k = khi - 32 + lane) and walks the rows j < khi - 1 RB at a time, warps taking
+// the row blocks of all segments round-robin.  f(j[RB], rowvalid[RB], k, pk) —
 // lane-level validity is rowvalid[u] && k > j[u].
-template <int T, bool CPLX, int DMAX, bool EXACT, class F>
-__device__ __forceinline__ void tiled_pairs(int N, int L, int LP, const double* __restrict__ phiC, F&& f) {
+template <int S, int RB, bool CPLX, int DMAX, bool EXACT, class F>
+__device__ __forceinline__ void tiled_pairs(int N, int len, int LP, const double* __restrict__ phiC, F&& f) {
   constexpr int LM = (CPLX ? 2 : 1) * DMAX;
-  constexpr int NWP = T / 32;
+  constexpr int NWP = S / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int g = 0;
   for (int khi = N; khi > 1; khi -= 32) {
     const int rows = khi - 1;  // j = 0 .. khi - 2
-    const int nb = (rows + 3) >> 2;
+    const int nb = (rows + RB - 1) / RB;
     const int k = khi - 32 + lane;
     int b = warp - (g % NWP);
     if (b < 0) b += NWP;
     if (b < nb) {
       double pk[LM];
-      load_col<LM, EXACT>(phiC + max(k, 0) * LP, pk, L);
+      load_col<LM, EXACT>(phiC + max(k, 0) * LP, pk, len);
       for (; b < nb; b += NWP) {
-        int j[4];
-        bool rv[4];
+        int j[RB];
+        bool rv[RB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          j[u] = 4 * b + u;
+        for (int u = 0; u < RB; ++u) {
+          j[u] = RB * b + u;
           rv[u] = j[u] < rows;
           if (!rv[u]) j[u] = rows - 1;
         }
@@ -251,7 +252,7 @@ __device__ int eval_cta_rt(const Prob& P, const double* __restrict__ x, const do
   // ---- phase 2: Gram upper triangle (smoothing.hpp:104-118): W <- x_p,
   // s = max x_p ((xv > smax) skips NaNs like the reference's std::max)
   double smax = -__longlong_as_double(0x7ff0000000000000LL);
-  tiled_pairs<T, CPLX, DMAX, EXACT>(N, C * d, LP, phiC, [&](const int* j, const bool* rv, int k, const double* pk) {
+  tiled_pairs<T, 4, CPLX, DMAX, EXACT>(N, C * d, LP, phiC, [&](const int* j, const bool* rv, int k, const double* pk) {
     double re[4], im[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -498,7 +499,7 @@ __device__ int coherence_cta_rt(const Prob& P, const double* __restrict__ f, boo
   if (zc != INT_MAX) return zc;
   double best = 0.0;
   long long arg = LLONG_MAX;
-  tiled_pairs<T, CPLX, DMAX, EXACT>(N, C * d, LP, sm.phiC, [&](const int* j, const bool* rv, int k, const double* pk) {
+  tiled_pairs<T, 4, CPLX, DMAX, EXACT>(N, C * d, LP, sm.phiC, [&](const int* j, const bool* rv, int k, const double* pk) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       double a[LM];

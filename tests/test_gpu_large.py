@@ -158,3 +158,20 @@ def test_large_solve_known_optimum_structure(ctx):
     for t in range(2):
         assert g["trials"][t].status == abi.TRIAL_OK
         assert g["trials"][t].coherence >= api.welch_bound(d, N) - 1e-9
+
+
+@pytest.mark.parametrize("field,d,N", [(R, 64, 1024), (C, 40, 300), (R, 33, 257)])
+def test_gradient_chunk_groups_same_bits(ctx, field, d, N):
+    """The gradient contraction walks the CAS k chunks inside a CTA when the batch alone fills the GPU
+    (one chunk group per request) and splits them over CTAs when it does not (up to one CTA per chunk,
+    csrc/bde_engine.cu chunk_groups): every grouping gives the oracle's bits."""
+    from paper_2207_06374_b200 import api
+    S = api.lanes(field, d, N)
+    x = orc.random_test_frame(field, d, N, 23)
+    Fo, so, go, _, zo = orc.eval_objective(field, d, N, S, x, 1e-2)
+    for B in (1, 3, 40):
+        pts = np.repeat(x[None], B, axis=0)
+        F, s, g, _, zc = ctx.eval_batch(field, d, N, pts, 1e-2)
+        for b in (0, B - 1):
+            assert zc[b] == -1 and bits(F[b]) == bits(Fo)
+            assert np.array_equal(bits(g[b]), bits(go))
