@@ -16,10 +16,11 @@
 //   bde_weights     w = exp((x - s)/delta) (x recomputed from G), z partial
 //                   per 16-row block
 //   bde_zreduce     z in block order, F = s + delta log z
-//   bde_grad        D^T = P^T Phi on DMMA with the coefficient matrix
+//   bde_grad_ws     D^T = P^T Phi on DMMA with the coefficient matrix
 //                   P(k, m) = (w/z) G(k, m) (conjugated below the diagonal)
 //                   formed tile by tile in shared memory from the packed
-//                   (w, G) — the N x N coefficient matrix never exists in HBM
+//                   (w, G) by producer warps while consumer warps run the
+//                   MMAs — the N x N coefficient matrix never exists in HBM
 //                   (north star: W o G fused into the contraction) — plus the
 //                   t chunk partials sum_k (w/z) u
 //   bde_finalize    chunk partials left to right, grad = ((acc - t phi)/alpha) 2
@@ -127,6 +128,36 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int NP>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NP) : "memory"); }
 
+// TMA bulk copies (cp.async.bulk, the copy engine — no tensor map needed for a
+// contiguous run) completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // D (m16 x n8, f64) += A (m16 x k4) B (k4 x n8): one DMMA, the ascending fma
 // chain over k per output.  a0 = A[g][t], a1 = A[g+8][t], b = B[t][g];
 // c0,c1 = C[g][2t, 2t+1], c2,c3 = C[g+8][2t, 2t+1]  (g = lane/4, t = lane%4).
@@ -206,17 +237,23 @@ __global__ void __launch_bounds__(NORM_T) bde_normalize(Pipe P) {
 // Upper-triangular 64x64 tile (jb <= kb) of G = Phi* Phi on DMMA.  8 warps:
 // warp (wj, wk) = (w / 4, w % 4) owns rows 32 wj .. +32 and columns 16 wk ..
 // +16: two m16 x two n8 MMA tiles, re (and im) accumulators.  Operands are
-// the columns of phi (rows of R^T), staged through shared memory by
-// cp.async in GKS-wide K stages, two buffers.
+// the columns of phi (rows of R^T), staged through shared memory in GKS-wide
+// K stages, two buffers.  TMA = true (L a multiple of 4): each stage is 128
+// bulk copies of one 256-byte row segment (cp.async.bulk, issued by warp 0,
+// four per lane) completing on the buffer's mbarrier — 128 copy instructions
+// per stage instead of 4096 8-byte cp.async; rows past N re-read row N - 1
+// (their products are never stored).  TMA = false: 8-byte cp.async with
+// zero fill, any L.
 // MODE 0: objective (packed G, block max of x); MODE 1: coherence (|G| by
 // hypot, first argmax of the tile).
 __host__ __device__ constexpr size_t bde_gram_smem() { return 2 * 2 * (size_t)BT * GSA * sizeof(double); }
 
-template <bool CPLX, int MODE>
+template <bool CPLX, int MODE, bool TMA>
 __global__ void __launch_bounds__(256, 2) bde_gram(Pipe P) {
   extern __shared__ __align__(16) double gsm[];  // [buf][A | B][64][GSA]
   __shared__ double red_v[8];
   __shared__ long long red_i[8];
+  __shared__ __align__(8) unsigned long long full_bar[2];
   const Shape& sh = P.sh;
   const int r = P.active[blockIdx.y];
   const Req q = P.reqs[r];
@@ -236,7 +273,32 @@ __global__ void __launch_bounds__(256, 2) bde_gram(Pipe P) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) re[a][b][e] = im[a][b][e] = 0.0;
   const int nst = (L + GKS - 1) / GKS;
+  if (TMA) {
+    if (tid == 0) {
+      mbar_init(&full_bar[0], 1);
+      mbar_init(&full_bar[1], 1);
+      fence_proxy_async();
+    }
+    __syncthreads();
+  }
   auto issue = [&](int s, int buf) {
+    if (TMA) {
+      if (warp == 0 && s < nst) {
+        double* As = gsm + buf * (2 * BT * GSA);
+        const int q0 = s * GKS;
+        const unsigned bytes = (unsigned)min(GKS, L - q0) * 8u;  // a multiple of 32 (L % 4 == 0)
+        if (lane == 0) mbar_expect_tx(&full_bar[buf], 2u * BT * bytes);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 2 * BT / 32; ++u) {
+          const int rr = lane + 32 * u;  // 0..63: A rows (jb), 64..127: B rows (kb)
+          const int row = rr & (BT - 1);
+          const int col = min((rr < BT ? jb : kb) * BT + row, N - 1);
+          bulk_g2s(As + rr * GSA, phi + (long long)col * L + q0, bytes, &full_bar[buf]);
+        }
+      }
+      return;
+    }
     if (s < nst) {
       double* As = gsm + buf * (2 * BT * GSA);
       double* Bs = As + BT * GSA;
@@ -255,8 +317,12 @@ __global__ void __launch_bounds__(256, 2) bde_gram(Pipe P) {
   issue(0, 0);
   for (int s = 0; s < nst; ++s) {
     issue(s + 1, (s + 1) & 1);
-    cpa_wait<1>();
-    __syncthreads();
+    if (TMA) {
+      mbar_wait(&full_bar[s & 1], (s >> 1) & 1);  // the stage's bytes have landed
+    } else {
+      cpa_wait<1>();
+      __syncthreads();
+    }
     const double* As = gsm + (s & 1) * (2 * BT * GSA);
     const double* Bs = As + BT * GSA;
     const int kq = min(GKS, L - s * GKS);  // valid K in this stage (zero-filled beyond)
@@ -288,7 +354,7 @@ __global__ void __launch_bounds__(256, 2) bde_gram(Pipe P) {
     }
     __syncthreads();
   }
-  cpa_wait<0>();
+  if (!TMA) cpa_wait<0>();
   // epilogue
   double best = 0.0;
   long long barg = LLONG_MAX;
@@ -440,221 +506,11 @@ __global__ void bde_zreduce(Pipe P) {
 }
 
 // ---------------------------------------------------------------- K5
-// D^T(m, i) = sum_k P(k, m) phi(i, k) over the k of chunk ch (ascending),
-// register-blocked on DMMA: rows m (64 per CTA), columns i (IB per CTA), 8
-// warps = 2 (m) x 4 (i).  Complex: one accumulator pair per (m, i); A = P^T
+// D^T(m, i) = sum_k P(k, m) phi(i, k) over the k of a CAS chunk (ascending),
+// register-blocked on DMMA.  Complex: one accumulator pair per (m, i); A = P^T
 // interleaved (pr, pi) per k, read as (pr, pi) for re and (pi, pr) for im;
-// B = phi interleaved, (fr, -fi) for re and (fr, fi) for im.  The P tile of a
-// stage is built from the packed (w, G) in registers one stage ahead (the
-// gather overlaps the MMAs) and stored to shared memory; the phi tile streams
-// in by cp.async.  i-block 0 also sums t_m = sum_k c u (ascending k, add).
-template <bool CPLX, int IB>
-struct GradCfg {
-  static constexpr int KK = CPLX ? 16 : 32;        // k per stage (interleaved K' = 32 either way)
-  static constexpr int KP = 32;                    // K' per stage
-  static constexpr int SA = KP + 4;                // P^T tile row stride (== 4 mod 16)
-  static constexpr int FW = CPLX ? 2 * IB : IB;    // doubles per phi row slice
-  static constexpr int SF = CPLX ? FW + 8 : FW + 4;  // == 8 / 4 mod 16: conflict-free fragments
-  static constexpr int NT = IB / 32;               // n8 tiles per warp (warp covers IB/4 columns)
-  static constexpr int A_D = BT * SA, F_D = KK * SF, CU_D = BT * KK;
-  static constexpr size_t smem = (size_t)(2 * A_D + 2 * F_D + CU_D) * sizeof(double);
-  static constexpr int EPT = BT * KK / 256;        // P elements gathered per thread per stage
-};
-
-template <bool CPLX, int IB>
-__global__ void __launch_bounds__(256, 1) bde_grad(Pipe P) {
-  using C = GradCfg<CPLX, IB>;
-  constexpr int KK = C::KK, SA = C::SA, SF = C::SF, FW = C::FW, NT = C::NT, EPT = C::EPT;
-  extern __shared__ __align__(16) double smem[];
-  double* Abuf = smem;                  // 2 x A_D
-  double* Fbuf = smem + 2 * C::A_D;     // 2 x F_D
-  double* CUs = Fbuf + 2 * C::F_D;      // CU_D
-  const Shape& sh = P.sh;
-  const int K = sh.K;
-  const int r = P.active[blockIdx.z / K], ch = blockIdx.z % K;
-  const Req q = P.reqs[r];
-  if (P.outs[r].zc != INT_MAX) return;
-  const int N = sh.N, L = sh.L, d = sh.d;
-  const int m0 = blockIdx.x * BT, i0 = blockIdx.y * IB;
-  const int k_lo = (int)(((long long)ch * N) / K), k_hi = (int)(((long long)(ch + 1) * N) / K);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wi = warp & 3;
-  const double* phi = P.ws.phi + (long long)q.slot * P.ws.s_phi;
-  const double* Gp = P.ws.G + (long long)q.slot * P.ws.s_G;
-  const double* Wp = P.ws.W + (long long)q.slot * P.ws.s_W;
-  const double z = P.outs[r].z;
-  const double yz = __drcp_rn(z);
-  const bool tsum = blockIdx.y == 0 && tid < BT;
-  double tacc = 0.0;
-
-  double re[2][NT][4], im[2][NT][4];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < NT; ++b)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) re[a][b][e] = im[a][b][e] = 0.0;
-
-  // ---- P tile gather (registers), one stage ahead
-  double rw[EPT], rgr[EPT], rgi[EPT];
-  int rk[EPT], rm[EPT];
-  auto gather = [&](int k0) {
-    // rows of a stage tile above the diagonal read along m, below it along k (coalesced both ways)
-    const bool upper = k0 + KK <= m0;
-#pragma unroll
-    for (int u = 0; u < EPT; ++u) {
-      const int e = tid + 256 * u;
-      const int mm = upper ? (e & (BT - 1)) : (e / KK);
-      const int kk = upper ? (e / BT) : (e % KK);
-      const int k = k0 + kk, m = m0 + mm;
-      rk[u] = kk;
-      rm[u] = mm;
-      rw[u] = 0.0;
-      rgr[u] = rgi[u] = 0.0;
-      if (k < k_hi && m < N && k != m) {
-        const long long p = k < m ? pair_index(k, m, N) : pair_index(m, k, N);
-        const double w = Wp[p];
-        rw[u] = w;
-        if (w != 0.0) {
-          if (CPLX) {
-            const double2 gg = *reinterpret_cast<const double2*>(Gp + 2 * p);
-            rgr[u] = gg.x;
-            rgi[u] = k < m ? gg.y : -gg.y;  // G(k, m) = conj(G(m, k)) below the diagonal
-          } else {
-            rgr[u] = Gp[p];
-          }
-        }
-      }
-    }
-  };
-  // coefficients c = w/z (Markstein == IEEE), P = c G, c u  -> shared memory
-  auto convert = [&](double* As) {
-#pragma unroll
-    for (int u = 0; u < EPT; ++u) {
-      double vr = 0.0, vi = 0.0, vu = 0.0;
-      if (rw[u] != 0.0) {
-        const double cq = div_rn(rw[u], z, yz);
-        if (cq != 0.0) {
-          const double gr = rgr[u], gi = rgi[u];
-          const double uu = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
-          double cc = cq;
-          if (!q.squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(uu), 1e-150)));
-          vr = __dmul_rn(cc, gr);
-          vi = __dmul_rn(cc, gi);
-          vu = __dmul_rn(cc, uu);
-        }
-      }
-      const int mm = rm[u], kk = rk[u];
-      if (CPLX) {
-        As[mm * SA + 2 * kk] = vr;
-        As[mm * SA + 2 * kk + 1] = vi;
-      } else {
-        As[mm * SA + kk] = vr;
-      }
-      CUs[mm * KK + kk] = vu;
-    }
-  };
-  auto issue_phi = [&](int k0, double* Fs) {
-    // rows kk: phi column k0 + kk, components [i0 * (CPLX ? 2 : 1), + FW)
-    const int c0 = CPLX ? 2 * i0 : i0;
-    for (int e = tid; e < KK * FW; e += 256) {
-      const int kk = e / FW, c = e - kk * FW;
-      const int k = k0 + kk;
-      const bool v = k < k_hi && c0 + c < L;
-      cpa8(Fs + kk * SF + c, phi + (v ? (long long)k * L + c0 + c : 0), v);
-    }
-    cpa_commit();
-  };
-
-  const int nst = (k_hi - k_lo + KK - 1) / KK;
-  if (nst > 0) {
-    issue_phi(k_lo, Fbuf);
-    gather(k_lo);
-    convert(Abuf);
-    cpa_wait<0>();
-    __syncthreads();
-  }
-  for (int s = 0; s < nst; ++s) {
-    const int k0 = k_lo + s * KK;
-    const int cur = s & 1;
-    const bool more = s + 1 < nst;
-    if (more) {
-      issue_phi(k0 + KK, Fbuf + (cur ^ 1) * C::F_D);
-      gather(k0 + KK);
-    }
-    if (tsum) {  // t chunk partial: ascending k, plain adds (c u of this stage)
-      const int kmax = min(KK, k_hi - k0);
-      for (int kk = 0; kk < kmax; ++kk) tacc = __dadd_rn(tacc, CUs[tid * KK + kk]);
-    }
-    const double* As = Abuf + cur * C::A_D;
-    const double* Fs = Fbuf + cur * C::F_D;
-#pragma unroll 2
-    for (int q4 = 0; q4 < C::KP; q4 += 4) {
-      double ar0[2], ar1[2], ai0[2], ai1[2];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int row = 32 * wm + 16 * mt + g;
-        ar0[mt] = As[row * SA + q4 + t];
-        ar1[mt] = As[(row + 8) * SA + q4 + t];
-        if (CPLX) {
-          ai0[mt] = As[row * SA + q4 + (t ^ 1)];
-          ai1[mt] = As[(row + 8) * SA + q4 + (t ^ 1)];
-        }
-      }
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int col = (IB / 4) * wi + 8 * nt + g;  // i within the block
-        double br, bi = 0.0;
-        if (CPLX) {
-          const int qq = q4 + t;  // interleaved K': k = qq / 2, component qq & 1
-          const double v = Fs[(qq >> 1) * SF + 2 * col + (qq & 1)];
-          br = (qq & 1) ? -v : v;
-          bi = v;
-        } else {
-          br = Fs[(q4 + t) * SF + col];
-        }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          dmma(re[mt][nt], ar0[mt], ar1[mt], br);
-          if (CPLX) dmma(im[mt][nt], ai0[mt], ai1[mt], bi);
-        }
-      }
-    }
-    __syncthreads();  // every thread is done with As[cur], Fs[cur] and CUs
-    if (more) {
-      convert(Abuf + (cur ^ 1) * C::A_D);
-      cpa_wait<0>();
-    }
-    __syncthreads();
-  }
-  // ---- outputs: chunk partials in the point layout
-  double* part = P.ws.part + (long long)q.slot * P.ws.s_part + (long long)ch * sh.dim;
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = m0 + 32 * wm + 16 * mt + g + 8 * h;
-        const int i = i0 + (IB / 4) * wi + 8 * nt + 2 * t;
-        if (m >= N) continue;
-        if (CPLX) {
-          double* o = part + (long long)m * L + 2 * i;  // 16-byte aligned (L and 2i even)
-          if (i < d) *reinterpret_cast<double2*>(o) = make_double2(re[mt][nt][2 * h], im[mt][nt][2 * h]);
-          if (i + 1 < d) *reinterpret_cast<double2*>(o + 2) = make_double2(re[mt][nt][2 * h + 1], im[mt][nt][2 * h + 1]);
-        } else {
-          double* o = part + (long long)m * L + i;
-          if (i < d) o[0] = re[mt][nt][2 * h];
-          if (i + 1 < d) o[1] = re[mt][nt][2 * h + 1];
-        }
-      }
-  if (tsum && m0 + tid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + tid] = tacc;
-}
-
-// ---------------------------------------------------------------- K5 (warp-specialised)
-// The same contraction as bde_grad with the work split by warp role, so the
-// tensor pipe never waits for the coefficient tiles:
+// B = phi interleaved, (fr, -fi) for re and (fr, fi) for im.  The work is split
+// by warp role, so the tensor pipe never waits for the coefficient tiles:
 //   * producer warps gather the packed (w, G) of a stage from HBM / L2, form
 //     c = w/z, P = c G (conjugated below the diagonal) and c u, store the P^T
 //     tile, and stream the phi tile in by 16-byte cp.async one stage ahead;

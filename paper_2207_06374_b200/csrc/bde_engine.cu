@@ -5,6 +5,7 @@
 #include <atomic>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -265,6 +266,32 @@ static cudaError_t launch_grad(const Pipe& P, int nreq, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Gram tiles.  Operand staging: 8-byte cp.async (default) or TMA bulk copies of the 256-byte row segments
+// (TRSTMI_GRAM_TMA=1, needs L % 4 == 0).  Measured on B200 (profiles/r2_gram_tma_vs_cpasync.txt): the bulk
+// variant is bit-identical and 28-38 % slower — 128 copies of 256 bytes per stage are bound by the copy
+// engine's per-request rate, not by bytes; a 2-D tensor map (one box per operand per stage) would need a
+// 16-byte swizzle that the f64 m16n8k4 fragment pattern turns into 2-way bank conflicts.
+static bool gram_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRSTMI_GRAM_TMA");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <int MODE>
+static cudaError_t launch_gram(const Pipe& P, int nreq, cudaStream_t st) {
+  const Shape& sh = P.sh;
+  const bool tma = gram_tma_enabled() && sh.L % 4 == 0;
+  const void* fn = sh.cplx ? (tma ? (const void*)bde_gram<true, MODE, true> : (const void*)bde_gram<true, MODE, false>)
+                           : (tma ? (const void*)bde_gram<false, MODE, true> : (const void*)bde_gram<false, MODE, false>);
+  const cudaError_t e = ensure_smem(fn, bde_gram_smem());
+  if (e != cudaSuccess) return e;
+  Pipe Pc = P;
+  void* args[] = {&Pc};
+  return cudaLaunchKernel(fn, dim3(sh.tiles, nreq), dim3(256), args, bde_gram_smem(), st);
+}
+
 // The evaluation pipeline over the requests listed in act (device), nreq of them.
 static int run_obj(Engine* E, const int* act, int nreq, bool any_wout, cudaStream_t st, std::string* err) {
   if (nreq <= 0) return TRSTMI_OK;
@@ -273,15 +300,9 @@ static int run_obj(Engine* E, const int* act, int nreq, bool any_wout, cudaStrea
   const int nc = bde_norm_cols(sh.L);
   BCHK(ensure_smem((const void*)bde_normalize, bde_norm_smem(sh.L)));
   bde_normalize<<<dim3((sh.N + nc - 1) / nc, nreq), NORM_T, bde_norm_smem(sh.L), st>>>(P);
-  if (sh.cplx) {
-    BCHK(ensure_smem((const void*)bde_gram<true, 0>, bde_gram_smem()));
-    bde_gram<true, 0><<<dim3(sh.tiles, nreq), 256, bde_gram_smem(), st>>>(P);
-    bde_weights<true><<<dim3(sh.nzb, nreq), BZLANES, 0, st>>>(P);
-  } else {
-    BCHK(ensure_smem((const void*)bde_gram<false, 0>, bde_gram_smem()));
-    bde_gram<false, 0><<<dim3(sh.tiles, nreq), 256, bde_gram_smem(), st>>>(P);
-    bde_weights<false><<<dim3(sh.nzb, nreq), BZLANES, 0, st>>>(P);
-  }
+  BCHK((launch_gram<0>(P, nreq, st)));
+  if (sh.cplx) bde_weights<true><<<dim3(sh.nzb, nreq), BZLANES, 0, st>>>(P);
+  else bde_weights<false><<<dim3(sh.nzb, nreq), BZLANES, 0, st>>>(P);
   bde_zreduce<<<nreq, 32, 0, st>>>(P);
   const int ib = ib_for(sh);
   cudaError_t e;
@@ -306,13 +327,7 @@ static int run_coh(Engine* E, const int* act, int nreq, cudaStream_t st, std::st
   const int nc = bde_norm_cols(sh.L);
   BCHK(ensure_smem((const void*)bde_normalize, bde_norm_smem(sh.L)));
   bde_normalize<<<dim3((sh.N + nc - 1) / nc, nreq), NORM_T, bde_norm_smem(sh.L), st>>>(P);
-  if (sh.cplx) {
-    BCHK(ensure_smem((const void*)bde_gram<true, 1>, bde_gram_smem()));
-    bde_gram<true, 1><<<dim3(sh.tiles, nreq), 256, bde_gram_smem(), st>>>(P);
-  } else {
-    BCHK(ensure_smem((const void*)bde_gram<false, 1>, bde_gram_smem()));
-    bde_gram<false, 1><<<dim3(sh.tiles, nreq), 256, bde_gram_smem(), st>>>(P);
-  }
+  BCHK((launch_gram<1>(P, nreq, st)));
   bde_coh_reduce<<<nreq, 256, 0, st>>>(P);
   g_launches += 3;
   BCHK(cudaGetLastError());

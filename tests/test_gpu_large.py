@@ -175,3 +175,32 @@ def test_gradient_chunk_groups_same_bits(ctx, field, d, N):
         for b in (0, B - 1):
             assert zc[b] == -1 and bits(F[b]) == bits(Fo)
             assert np.array_equal(bits(g[b]), bits(go))
+
+
+def test_gram_tma_variant_same_bits():
+    """TRSTMI_GRAM_TMA=1 stages the Gram operands with TMA bulk copies (cp.async.bulk + mbarrier) instead of
+    cp.async; the variant is chosen once per process, so it runs in a child process: same bits as the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from paper_2207_06374_b200 import abi, api
+from tests import oracle_ffi as orc
+ctx = api.Context(0)
+for field, d, N in ((abi.COMPLEX, 32, 64), (abi.REAL, 64, 128), (abi.COMPLEX, 24, 70)):
+    S = api.lanes(field, d, N)
+    x = orc.random_test_frame(field, d, N, 41)
+    F, s, g, _, zc = ctx.eval_batch(field, d, N, x[None], 1e-2)
+    Fo, so, go, _, zo = orc.eval_objective(field, d, N, S, x, 1e-2)
+    assert F[0] == Fo and np.array_equal(g[0].view(np.uint64), go.view(np.uint64)), (field, d, N)
+    mu, arg, _ = ctx.coherence_batch(field, d, N, x[None], True)
+    mo, ao, _ = orc.coherence(field, d, N, x, True)
+    assert mu[0] == mo and arg[0] == ao
+print("tma ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TRSTMI_GRAM_TMA="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "tma ok" in r.stdout, r.stdout + r.stderr
