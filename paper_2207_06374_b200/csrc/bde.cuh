@@ -527,19 +527,33 @@ template <bool CPLX, int IB>
 struct GradWsCfg {
   static constexpr int KK = CPLX ? 16 : 32;
   static constexpr int KP = 32;
-  static constexpr int SA = KP + 4;
+  // P^T tile rows: complex 36 doubles (== 4 mod 16: conflict-free fragment loads); real 32 doubles with the
+  // column index XOR-swizzled by the row (aswz) — conflict-free for the fragment loads AND for the producers'
+  // stores in both tile orientations (lanes along k, or along m: a padded stride is 4-way conflicted there)
+  static constexpr int SA = CPLX ? KP + 4 : KP;
   static constexpr int FW = CPLX ? 2 * IB : IB;
   static constexpr int SF = CPLX ? FW + 8 : FW + 4;
   static constexpr int WI = 4;                                 // consumer warps along i
   static constexpr int WM = (CPLX && IB >= 128) ? 4 : 2;       // ... along m
   static constexpr int MT = BT / (16 * WM), NT = IB / (8 * WI);
-  static constexpr int A_D = BT * SA, F_D = KK * SF, CU_D = BT * KK;
+  static constexpr int SU = KK + 1;  // c u row stride: the t sums read one row per lane (odd: conflict-free)
+  static constexpr int A_D = BT * SA, F_D = KK * SF, CU_D = BT * SU;
   static constexpr int NST = 3;
   static constexpr int NPROD = CPLX ? 128 : 256;  // real stages hold twice the k
-  static constexpr int NCONS = 32 * WM * WI, NTHR = NPROD + NCONS;
-  static constexpr size_t smem = (size_t)(NST * (A_D + F_D) + 2 * CU_D) * sizeof(double);
+  static constexpr int NCONS = 32 * WM * WI;
+  // real frames (a P element feeds only d MMAs' worth of work): the producers are the critical path, so the
+  // t sums move to two warps of their own — they consume the c u tile of a stage like the MMA warps consume
+  // the P^T tile (1054 -> 902 us per 108 requests at config 4; gathering (w, G) two stages ahead into a second
+  // register set was slower: 1167 us, profiles/r2_bde_grad_ws.txt)
+  static constexpr int NTW = CPLX ? 0 : BT;
+  static constexpr int NTHR = NPROD + NCONS + NTW;
+  static constexpr int NCU = NTW ? NST : 2;  // c u tiles: one per stage buffer when the t warps consume them
+  static constexpr size_t smem = (size_t)(NST * (A_D + F_D) + NCU * CU_D) * sizeof(double);
   static constexpr int EPT = BT * KK / NPROD;
 };
+
+// XOR swizzle of the real P^T tile: row bits 0-1 into column bits 2-3, row bits 2-3 into column bits 0-1
+__device__ __forceinline__ int aswz(int row) { return ((row & 3) << 2) | ((row >> 2) & 3); }
 
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
@@ -551,13 +565,13 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 template <bool CPLX, int IB>
 __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe P, int KS) {
   using C = GradWsCfg<CPLX, IB>;
-  constexpr int KK = C::KK, SA = C::SA, SF = C::SF, FW = C::FW, MT = C::MT, NT = C::NT, EPT = C::EPT, NST = C::NST;
+  constexpr int KK = C::KK, SA = C::SA, SF = C::SF, SU = C::SU, FW = C::FW, MT = C::MT, NT = C::NT, EPT = C::EPT, NST = C::NST;
   constexpr int NPROD = C::NPROD, NTHR = C::NTHR, WM = C::WM, WI = C::WI;
   constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + NST, BAR_PROD = 1 + 2 * NST;
   extern __shared__ __align__(16) double smem[];
   double* Abuf = smem;                       // NST x A_D
   double* Fbuf = smem + NST * C::A_D;        // NST x F_D
-  double* CUbuf = Fbuf + NST * C::F_D;       // 2 x CU_D
+  double* CUbuf = Fbuf + NST * C::F_D;       // NCU x CU_D
   const Shape& sh = P.sh;
   const int K = sh.K;
   const int r = P.active[blockIdx.z / KS], cg = blockIdx.z % KS;
@@ -579,7 +593,10 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
     const double z = P.outs[r].z;
     const double yz = __drcp_rn(z);
     const bool tsum = blockIdx.y == 0 && tid < BT;
-    double rw[EPT], rgr[EPT], rgi[EPT];  // the packed (w, G) of the stage to convert next
+    struct RegSet {
+      double w[EPT], gr[EPT], gi[EPT];
+    };
+    RegSet setA;  // the packed (w, G) of the stage to convert next
     auto elem = [&](int k0, int u, int& mm, int& kk) {
       // rows of a stage tile above the diagonal read along m, else along k (coalesced both ways)
       const bool upper = k0 + KK <= m0;
@@ -587,7 +604,7 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
       mm = upper ? (e & (BT - 1)) : (e / KK);
       kk = upper ? (e / BT) : (e % KK);
     };
-    auto gather = [&](int k0, int k_hi) {
+    auto gather = [&](int k0, int k_hi, RegSet& R) {
 #pragma unroll
       for (int u = 0; u < EPT; ++u) {
         int mm, kk;
@@ -606,23 +623,46 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
             gr = Gp[p];
           }
         }
-        rw[u] = w;
-        rgr[u] = gr;
-        rgi[u] = gi;
+        R.w[u] = w;
+        R.gr[u] = gr;
+        R.gi[u] = gi;
       }
     };
-    auto convert = [&](int k0, double* As, double* CUs) {
+    auto convert = [&](int k0, const RegSet& R, double* As, double* CUs) {
+      if constexpr (!CPLX) {
+        // real frames hold twice the k per stage and feed half the MMAs per element: the conversion is the
+        // producers' critical path, so it is branch-free (the EPT quotient chains interleave); the rare
+        // operands the Markstein quotient cannot take (0 < |w| < 2^-900) and the magnitude mode take the
+        // general loop below
+        bool plain = q.squared != 0;
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) plain &= !(R.w[u] != 0.0 && fabs(R.w[u]) < 0x1.0p-900);
+        if (plain) {
+#pragma unroll
+          for (int u = 0; u < EPT; ++u) {
+            int mm, kk;
+            elem(k0, u, mm, kk);
+            const double cq = div_fast(R.w[u], z, yz);  // w == 0 -> +0
+            const double gr = R.gr[u];
+            const double uu = __dmul_rn(gr, gr);
+            const bool nz = cq != 0.0;  // an underflowed quotient contributes exact zeros
+            As[mm * SA + (kk ^ aswz(mm))] = nz ? __dmul_rn(cq, gr) : 0.0;
+            CUs[mm * SU + kk] = nz ? __dmul_rn(cq, uu) : 0.0;
+          }
+          return;
+        }
+      }
 #pragma unroll
       for (int u = 0; u < EPT; ++u) {
         int mm, kk;
         elem(k0, u, mm, kk);
         double vr = 0.0, vi = 0.0, vu = 0.0;
-        const double w = rw[u];
+        const double w = R.w[u];
         if (w != 0.0) {
           const double cq = div_rn(w, z, yz);
           if (cq != 0.0) {
             // G(k, m) = conj(G(m, k)) below the diagonal (k > m: the packed entry is G(m, k))
-            const double gr = rgr[u], gi = (k0 + kk < m0 + mm) ? rgi[u] : -rgi[u];
+            const double gr = R.gr[u], gi = (k0 + kk < m0 + mm) ? R.gi[u] : -R.gi[u];
             const double uu = CPLX ? __dadd_rn(__dmul_rn(gr, gr), __dmul_rn(gi, gi)) : __dmul_rn(gr, gr);
             double cc = cq;
             if (!q.squared) cc = __dmul_rn(cc, __ddiv_rn(0.5, fmax(sqrt(uu), 1e-150)));
@@ -634,9 +674,9 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
         if (CPLX) {
           *reinterpret_cast<double2*>(As + mm * SA + 2 * kk) = make_double2(vr, vi);
         } else {
-          As[mm * SA + kk] = vr;
+          As[mm * SA + (kk ^ aswz(mm))] = vr;
         }
-        CUs[mm * KK + kk] = vu;
+        CUs[mm * SU + kk] = vu;
       }
     };
     auto issue_phi = [&](int k0, int k_hi, double* Fs) {
@@ -659,53 +699,98 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
         }
       }
     };
-    // stage (ch, s) -> the next stage, across chunk ends
-    auto next_stage = [&](int ch, int s, int& ch2, int& s2) {
-      const int nst = (chunk_lo(ch + 1) - chunk_lo(ch) + KK - 1) / KK;
-      ch2 = ch;
-      s2 = s + 1;
-      if (s2 >= nst) {
-        ch2 = ch + 1;
-        s2 = 0;
-      }
-      return ch2 < ch_hi;
+    // stage iterator over the chunks of this CTA
+    struct It {
+      int ch, s;
     };
-    int gs = 0;  // global stage counter (buffer cycling)
+    auto nst_of = [&](int ch) { return (chunk_lo(ch + 1) - chunk_lo(ch) + KK - 1) / KK; };
+    auto advance = [&](It it) {
+      ++it.s;
+      if (it.s >= nst_of(it.ch)) {
+        ++it.ch;
+        it.s = 0;
+      }
+      return it;
+    };
+    auto valid = [&](It it) { return it.ch < ch_hi; };
+    auto k0_of = [&](It it) { return chunk_lo(it.ch) + it.s * KK; };
+    auto khi_of = [&](It it) { return chunk_lo(it.ch + 1); };
     // prologue: the first stage's phi tile and packed (w, G) in flight
-    issue_phi(chunk_lo(ch_lo), chunk_lo(ch_lo + 1), Fbuf);
+    It cur{ch_lo, 0};
+    issue_phi(k0_of(cur), khi_of(cur), Fbuf);
     cpa_commit();
-    gather(chunk_lo(ch_lo), chunk_lo(ch_lo + 1));
+    gather(k0_of(cur), khi_of(cur), setA);
+    double tacc = 0.0;
+    for (int gs = 0; valid(cur); ++gs) {
+      const It n1 = advance(cur);
+      const int k0 = k0_of(cur), k_hi = khi_of(cur);
+      const int b = gs % NST, b2 = (gs + 1) % NST;
+      const bool more = valid(n1);
+      auto stage = [&](RegSet& R) {
+        // the next stage's phi tile streams in while this stage is converted
+        if (more) {
+          if (gs + 1 >= NST) nbar_sync(BAR_EMPTY + b2, NTHR);  // its readers are done with buffer b2
+          issue_phi(k0_of(n1), khi_of(n1), Fbuf + b2 * C::F_D);
+        }
+        cpa_commit();
+        double* CUs = CUbuf + (C::NTW ? b : (gs & 1)) * C::CU_D;
+        convert(k0, R, Abuf + b * C::A_D, CUs);
+        cpa_wait<1>();  // this stage's phi tile (committed one iteration ago) has landed
+        __threadfence_block();
+        nbar_arrive(BAR_FULL + b, NTHR);
+        if (more) gather(k0_of(n1), khi_of(n1), R);  // the next stage's (w, G): lands during the MMAs
+        if constexpr (C::NTW == 0) {
+          nbar_sync(BAR_PROD, NPROD);  // CUs complete (and the previous stage's t sums read)
+          if (tsum) {  // t chunk partial: ascending k, plain adds (c u of this stage); loads first, then the chain
+            const int kmax = min(KK, k_hi - k0);
+            double cu[KK];
+#pragma unroll
+            for (int kk = 0; kk < KK; ++kk) cu[kk] = CUs[tid * SU + kk];
+#pragma unroll
+            for (int kk = 0; kk < KK; ++kk)
+              if (kk < kmax) tacc = __dadd_rn(tacc, cu[kk]);
+          }
+        }
+      };
+      stage(setA);
+      if constexpr (C::NTW == 0) {
+        if (!more || n1.ch != cur.ch) {  // chunk end
+          if (tsum && m0 + tid < N)
+            P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)cur.ch * N + m0 + tid] = tacc;
+          tacc = 0.0;
+        }
+      }
+      cur = n1;
+    }
+    cpa_wait<0>();
+  } else if (C::NTW > 0 && tid >= NPROD + C::NCONS) {
+    // ======================================================= t warps (real frames)
+    // t_m = sum_k c u over each chunk, ascending k, plain adds: thread ttid owns row m0 + ttid and consumes the
+    // c u tile of every stage buffer like the MMA warps consume the P^T tile
+    const int ttid = tid - NPROD - C::NCONS;
+    const bool tsum = blockIdx.y == 0;
+    int gs = 0;
     for (int ch = ch_lo; ch < ch_hi; ++ch) {
       const int k_lo = chunk_lo(ch), k_hi = chunk_lo(ch + 1);
       const int nst = (k_hi - k_lo + KK - 1) / KK;
       double tacc = 0.0;
       for (int s = 0; s < nst; ++s, ++gs) {
-        const int k0 = k_lo + s * KK;
         const int b = gs % NST;
-        int ch2, s2;
-        const bool more = next_stage(ch, s, ch2, s2);
-        const int b2 = (gs + 1) % NST;
-        // the next stage's phi tile streams in while this stage is converted
-        if (more) {
-          if (gs + 1 >= NST) nbar_sync(BAR_EMPTY + b2, NTHR);  // consumers are done with buffer b2
-          issue_phi(chunk_lo(ch2) + s2 * KK, chunk_lo(ch2 + 1), Fbuf + b2 * C::F_D);
+        nbar_sync(BAR_FULL + b, NTHR);
+        if (tsum) {
+          const double* CUs = CUbuf + b * C::CU_D;
+          const int kmax = min(KK, k_hi - (k_lo + s * KK));
+          double cu[KK];
+#pragma unroll
+          for (int kk = 0; kk < KK; ++kk) cu[kk] = CUs[ttid * SU + kk];
+#pragma unroll
+          for (int kk = 0; kk < KK; ++kk)
+            if (kk < kmax) tacc = __dadd_rn(tacc, cu[kk]);
         }
-        cpa_commit();
-        double* CUs = CUbuf + (gs & 1) * C::CU_D;
-        convert(k0, Abuf + b * C::A_D, CUs);
-        cpa_wait<1>();  // this stage's phi tile (committed one iteration ago) has landed
-        __threadfence_block();
-        nbar_arrive(BAR_FULL + b, NTHR);
-        if (more) gather(chunk_lo(ch2) + s2 * KK, chunk_lo(ch2 + 1));  // lands during the consumers' stage
-        nbar_sync(BAR_PROD, NPROD);  // CUs complete (and the previous stage's t sums read)
-        if (tsum) {  // t chunk partial: ascending k, plain adds (c u of this stage)
-          const int kmax = min(KK, k_hi - k0);
-          for (int kk = 0; kk < kmax; ++kk) tacc = __dadd_rn(tacc, CUs[tid * KK + kk]);
-        }
+        nbar_arrive(BAR_EMPTY + b, NTHR);
       }
-      if (tsum && m0 + tid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + tid] = tacc;
+      if (tsum && m0 + ttid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + ttid] = tacc;
     }
-    cpa_wait<0>();
   } else {
     // ======================================================= consumers
     const int ctid = tid - NPROD, lane = ctid & 31, warp = ctid >> 5;
@@ -734,8 +819,13 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
             const int row = rbase + 16 * mt + g;
-            ar0[mt] = As[row * SA + q4 + t];
-            ar1[mt] = As[(row + 8) * SA + q4 + t];
+            if (CPLX) {
+              ar0[mt] = As[row * SA + q4 + t];
+              ar1[mt] = As[(row + 8) * SA + q4 + t];
+            } else {
+              ar0[mt] = As[row * SA + ((q4 + t) ^ aswz(row))];
+              ar1[mt] = As[(row + 8) * SA + ((q4 + t) ^ aswz(row + 8))];
+            }
             if (CPLX) {
               ai0[mt] = As[row * SA + q4 + (t ^ 1)];
               ai1[mt] = As[(row + 8) * SA + q4 + (t ^ 1)];
