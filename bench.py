@@ -8,9 +8,13 @@ from random_frame(SplitMix64(mix_seed(0, i)))), each a full anneal() with
 TrustRegionConfig.max_outer = 500 (stage k capped at 500 + 50k, solver.hpp:187),
 default delta schedule at eps_target 1e-7 (8 stages).
 
-A step is the full anneal of one slice of the config's trials (default 1024
-trials for config 2, so 4 consecutive steps cover the 4096 trials once; the
-driver's 20 steps cover them 5 times).  Warm-up steps anneal one SM-wave of
+A step is the full anneal of one slice of the config's trials (default 2048
+trials for config 2, so 2 consecutive steps cover the 4096 trials once; the
+driver's 20 steps cover them 10 times; ~37 s per step, so the driver's
+--steps 20 --warmup 5 run takes ~15 minutes with the CPU baseline).  A
+wall-clock guard (--budget-s, default 1500 s) stops the timed loop early
+rather than lose the line: "steps" then reports the steps actually timed and
+"steps_requested" the K that was asked for.  Warm-up steps anneal one SM-wave of
 trials (there is no JIT/autotune state to warm).  `e2e` repeats slice 0
 through the host-pointer C ABI (trstmi_solve_batch: H2D of start frames and
 generator states, D2H of parameters, frames and records inside the timed
@@ -56,7 +60,7 @@ CONFIGS = {
     #   "stage0": the anneal's first stage (delta = 0.1) with that max_outer —
     #             the fixed-work mode SURVEY.md §8d prescribes for configs 4-5
     "c1": (abi.REAL, 4, 10, 64, 200, "anneal", 64),
-    "c2": (abi.COMPLEX, 2, 100, 4096, 500, "anneal", 1024),
+    "c2": (abi.COMPLEX, 2, 100, 4096, 500, "anneal", 2048),
     "c3": (abi.COMPLEX, 6, 36, 1024, 1000, "anneal", 1024),
     "c4": (abi.REAL, 64, 1024, 256, 300, "stage0", 256),
     "c5": (abi.COMPLEX, 128, 4096, 64, 100, "stage0", 64),
@@ -278,6 +282,7 @@ def cpu_baseline(args, field, d, N, workload):
 
 # ---------------------------------------------------------------------------- GPU arm
 def main():
+    t_start = time.perf_counter()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=4)
@@ -290,6 +295,8 @@ def main():
     ap.add_argument("--cpu-trials", type=int, default=0)
     ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds cap of the cpu_baseline cycle")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--budget-s", type=float, default=1500.0,
+                    help="wall-clock guard: stop the timed loop (and skip the CPU baseline) rather than exceed this")
     ap.add_argument("--cpu-outer", type=int, default=0,
                     help="stage0 configs: outer iterations per CPU sample trial (default 2; 1 when N > 2048)")
     args = ap.parse_args()
@@ -395,12 +402,24 @@ def main():
     torch.cuda.synchronize()
     times, outers, evals_l = [], [], []
     for i in range(args.steps):
+        if times:  # wall-clock guard: this step, the e2e pass and the CPU baseline must still fit
+            left = args.budget_s - (time.perf_counter() - t_start)
+            need = 2.2 * max(times) + (0 if args.no_cpu or world > 1 else min(args.cpu_budget, 60.0))
+            if world > 1:  # every rank must take the same decision
+                f = torch.tensor([1.0 if left < need else 0.0], device="cuda")
+                dist.all_reduce(f, op=dist.ReduceOp.MAX)
+                stop = f.item() > 0
+            else:
+                stop = left < need
+            if stop:
+                break
         s = i % n_slices
         lo = s * slc
         t, o, e = device_step(lo, min(slc, count - lo))
         times.append(t)
         outers.append(o)
         evals_l.append(e)
+    steps_done = len(times)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -478,12 +497,16 @@ def main():
 
     cpu = None
     if not args.no_cpu and world == 1:
-        cpu = cpu_baseline(args, field, d, N, workload)
+        left = args.budget_s - (time.perf_counter() - t_start)
+        if left > 30.0:
+            args.cpu_budget = min(args.cpu_budget, max(left - 20.0, 10.0))
+            cpu = cpu_baseline(args, field, d, N, workload)
 
     value = tot_outer_all / t_all
     line = {
-        "metric": METRIC, "value": value, "unit": "TR iterations/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": "TR iterations/s", "n_gpus": world, "steps": steps_done,
+        "steps_requested": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_all / max(steps_done, 1), "higher_is_better": True,
         "scaling": "strong" if (sharded_frame or args.scaling == "strong") else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "gram_entries_per_s": tot_evals_all * n / t_all, "evals_per_s": tot_evals_all / t_all,

@@ -204,3 +204,22 @@ print("tma ok")
     env = dict(os.environ, TRSTMI_GRAM_TMA="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "tma ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_config4_full_size_trajectory_bit_exact(ctx):
+    """BASELINE config 4 at full size (real d = 64, N = 1024): two trials through the first trust-region
+    iterations of stage 0 on the batched device engine — every OuterRecord, CG exit and count identical to the
+    oracle (the oracle needs ~0.5 s per evaluation at this size, hence the short budget)."""
+    from paper_2207_06374_b200 import api
+    from tests.test_gpu_parity import _cmp_solve
+    field, d, N = R, 64, 1024
+    cfg = abi.default_cfg(field, d, N, 6)
+    cfg.n_stages = 1
+    cfg.schedule[0] = api.default_schedule(N)[0]
+    cfg.record_cap = 16
+    S = api.lanes(field, d, N)
+    starts, st = api.random_frames(field, d, N, 0, 0, 2)
+    g = ctx.solve_batch(cfg, starts, st)
+    o = orc.solve_batch(cfg, S, starts, st, threads=2)
+    assert g["trials"][0].outer_iterations == 6
+    _cmp_solve(g, o, 2, 1, 16)

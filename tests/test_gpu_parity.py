@@ -179,6 +179,22 @@ def test_solve_batch_trajectory_bit_exact(ctx, field, d, N, trials, max_outer, c
     _cmp_solve(g, o, trials, g["n_stages"], cap)
 
 
+@pytest.mark.parametrize("field,d,N,trials,max_outer", [
+    (C, 6, 36, 4, 1000),   # BASELINE config 3: the config's full budget (8 stages, max_outer 1000 + 50k)
+    (C, 2, 100, 4, 500),   # BASELINE config 2: the config's full budget (~2.5e5 evaluations per trial)
+])
+def test_full_budget_trajectories_bit_exact(ctx, field, d, N, trials, max_outer):
+    """Whole anneals at the headline configs' own budgets: every stage record, iteration / evaluation /
+    HVP count, final parameters and frames identical to the oracle (~50 s of CPU oracle time)."""
+    from paper_2207_06374_b200 import api
+    cfg = abi.default_cfg(field, d, N, max_outer)
+    S = api.lanes(field, d, N)
+    starts, st = api.random_frames(field, d, N, 0, 0, trials)
+    g = ctx.solve_batch(cfg, starts, st)
+    o = orc.solve_batch(cfg, S, starts, st, threads=trials)
+    _cmp_solve(g, o, trials, g["n_stages"], 0)
+
+
 def test_stage_boundary_rescue(ctx):
     # test_solver.cpp:232-250: column 2 is zero; with a generator the anneal
     # recovers, without one the restart fails with ZeroColumnError(2)
