@@ -308,6 +308,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if world > 1:  # the communicator's ranks / transport (NVLink, NVLS) are countable in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     import torch
     import torch.distributed as dist

@@ -256,11 +256,10 @@ static int chunk_groups(const Shape& sh, int ib, int nreq) {
 }
 
 template <bool CPLX, int IB>
-static cudaError_t launch_grad(const Pipe& P, int nreq, cudaStream_t st) {
+static cudaError_t launch_grad(const Pipe& P, int nreq, int KS, cudaStream_t st) {
   using C = GradWsCfg<CPLX, IB>;
   const cudaError_t e = ensure_smem((const void*)bde_grad_ws<CPLX, IB>, C::smem);
   if (e != cudaSuccess) return e;
-  const int KS = chunk_groups(P.sh, IB, nreq);
   dim3 grid((P.sh.N + BT - 1) / BT, (P.sh.d + IB - 1) / IB, KS * nreq);
   bde_grad_ws<CPLX, IB><<<grid, C::NTHR, C::smem, st>>>(P, KS);
   return cudaGetLastError();
@@ -305,12 +304,14 @@ static int run_obj(Engine* E, const int* act, int nreq, bool any_wout, cudaStrea
   else bde_weights<false><<<dim3(sh.nzb, nreq), BZLANES, 0, st>>>(P);
   bde_zreduce<<<nreq, 32, 0, st>>>(P);
   const int ib = ib_for(sh);
+  const int KS = chunk_groups(sh, ib, nreq);
   cudaError_t e;
-  if (sh.cplx) e = ib == 128 ? launch_grad<true, 128>(P, nreq, st) : ib == 64 ? launch_grad<true, 64>(P, nreq, st)
-                                                                              : launch_grad<true, 32>(P, nreq, st);
-  else e = ib == 64 ? launch_grad<false, 64>(P, nreq, st) : launch_grad<false, 32>(P, nreq, st);
+  if (sh.cplx) e = ib == 128 ? launch_grad<true, 128>(P, nreq, KS, st) : ib == 64 ? launch_grad<true, 64>(P, nreq, KS, st)
+                                                                                  : launch_grad<true, 32>(P, nreq, KS, st);
+  else e = ib == 64 ? launch_grad<false, 64>(P, nreq, KS, st) : launch_grad<false, 32>(P, nreq, KS, st);
   BCHK(e);
-  bde_finalize<<<dim3((unsigned)((sh.dim + 255) / 256), nreq), 256, 0, st>>>(P);
+  // one chunk group: the contraction folded the chunk partials (CAS order) into slot 0
+  bde_finalize<<<dim3((unsigned)((sh.dim + 255) / 256), nreq), 256, 0, st>>>(P, KS == 1 ? 1 : sh.K);
   g_launches += 6;
   if (any_wout) {
     bde_wout<<<dim3(256, nreq), 256, 0, st>>>(P);
