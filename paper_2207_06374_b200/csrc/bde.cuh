@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
     issue_phi(k0_of(cur), khi_of(cur), Fbuf);
     cpa_commit();
     gather(k0_of(cur), khi_of(cur), setA);
-    double tacc = 0.0, ttot = 0.0;
+    double tacc = 0.0;
     for (int gs = 0; valid(cur); ++gs) {
       const It n1 = advance(cur);
       const int k0 = k0_of(cur), k_hi = khi_of(cur);
@@ -755,13 +755,9 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
       };
       stage(setA);
       if constexpr (C::NTW == 0) {
-        if (!more || n1.ch != cur.ch) {  // chunk end (KS == 1: the chunk partials fold left to right into slot 0)
-          if (KS == 1) {
-            ttot = cur.ch == ch_lo ? tacc : __dadd_rn(ttot, tacc);
-            if (!more && tsum && m0 + tid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + m0 + tid] = ttot;
-          } else if (tsum && m0 + tid < N) {
+        if (!more || n1.ch != cur.ch) {  // chunk end
+          if (tsum && m0 + tid < N)
             P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)cur.ch * N + m0 + tid] = tacc;
-          }
           tacc = 0.0;
         }
       }
@@ -775,7 +771,6 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
     const int ttid = tid - NPROD - C::NCONS;
     const bool tsum = blockIdx.y == 0;
     int gs = 0;
-    double ttot = 0.0;
     for (int ch = ch_lo; ch < ch_hi; ++ch) {
       const int k_lo = chunk_lo(ch), k_hi = chunk_lo(ch + 1);
       const int nst = (k_hi - k_lo + KK - 1) / KK;
@@ -795,12 +790,7 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
         }
         nbar_arrive(BAR_EMPTY + b, NTHR);
       }
-      if (KS == 1) {
-        ttot = ch == ch_lo ? tacc : __dadd_rn(ttot, tacc);
-        if (ch + 1 == ch_hi && tsum && m0 + ttid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + m0 + ttid] = ttot;
-      } else if (tsum && m0 + ttid < N) {
-        P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + ttid] = tacc;
-      }
+      if (tsum && m0 + ttid < N) P.ws.tpart[(long long)q.slot * P.ws.s_tpart + (long long)ch * N + m0 + ttid] = tacc;
     }
   } else {
     // ======================================================= consumers
@@ -863,11 +853,10 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
         }
         nbar_arrive(BAR_EMPTY + b, NTHR);
       }
-      // ---- this chunk's partial, point layout.  A CTA that walks ALL chunks (KS == 1) folds them left to
-      // right into slot 0 as it goes — the CAS combine order, one (L2-resident) array instead of K
-      const bool fold = KS == 1;
-      double* part = P.ws.part + (long long)q.slot * P.ws.s_part + (fold ? 0LL : (long long)ch * sh.dim);
-      const bool add = fold && ch > ch_lo;
+      // ---- this chunk's partial, point layout.  (Folding the chunk partials left to right into one array
+      // here — a read-modify-write at every chunk end — was measured: finalize 117 -> 61 us but this kernel
+      // 5580 -> 6067 us per 8 config-5 requests; the K partials stay separate.)
+      double* part = P.ws.part + (long long)q.slot * P.ws.s_part + (long long)ch * sh.dim;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -879,26 +868,13 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
             if (m >= N) continue;
             if (CPLX) {
               double* o = part + (long long)m * L + 2 * i;  // 16-byte aligned (L and 2i even)
-              if (i < d) {
-                double2 v = make_double2(re[mt][nt][2 * h], im[mt][nt][2 * h]);
-                if (add) {  // this thread wrote the running sum itself: no other reader or writer
-                  const double2 pv = *reinterpret_cast<const double2*>(o);
-                  v = make_double2(__dadd_rn(pv.x, v.x), __dadd_rn(pv.y, v.y));
-                }
-                *reinterpret_cast<double2*>(o) = v;
-              }
-              if (i + 1 < d) {
-                double2 v = make_double2(re[mt][nt][2 * h + 1], im[mt][nt][2 * h + 1]);
-                if (add) {
-                  const double2 pv = *reinterpret_cast<const double2*>(o + 2);
-                  v = make_double2(__dadd_rn(pv.x, v.x), __dadd_rn(pv.y, v.y));
-                }
-                *reinterpret_cast<double2*>(o + 2) = v;
-              }
+              if (i < d) *reinterpret_cast<double2*>(o) = make_double2(re[mt][nt][2 * h], im[mt][nt][2 * h]);
+              if (i + 1 < d)
+                *reinterpret_cast<double2*>(o + 2) = make_double2(re[mt][nt][2 * h + 1], im[mt][nt][2 * h + 1]);
             } else {
               double* o = part + (long long)m * L + i;
-              if (i < d) o[0] = add ? __dadd_rn(o[0], re[mt][nt][2 * h]) : re[mt][nt][2 * h];
-              if (i + 1 < d) o[1] = add ? __dadd_rn(o[1], re[mt][nt][2 * h + 1]) : re[mt][nt][2 * h + 1];
+              if (i < d) o[0] = re[mt][nt][2 * h];
+              if (i + 1 < d) o[1] = re[mt][nt][2 * h + 1];
             }
           }
     }
@@ -906,7 +882,7 @@ __global__ void __launch_bounds__(GradWsCfg<CPLX, IB>::NTHR, 1) bde_grad_ws(Pipe
 }
 
 // ---------------------------------------------------------------- K6
-__global__ void bde_finalize(Pipe P, int nparts) {  // nparts: K chunk partials, or 1 when the contraction folded them
+__global__ void bde_finalize(Pipe P) {
   const Shape& sh = P.sh;
   const int r = P.active[blockIdx.y];
   const Req q = P.reqs[r];
@@ -920,7 +896,7 @@ __global__ void bde_finalize(Pipe P, int nparts) {  // nparts: K chunk partials,
   const double* part = P.ws.part + (long long)q.slot * P.ws.s_part;
   const double* tpart = P.ws.tpart + (long long)q.slot * P.ws.s_tpart;
   double a = part[e], tt = tpart[m];
-  for (int ch = 1; ch < nparts; ++ch) {
+  for (int ch = 1; ch < sh.K; ++ch) {
     a = __dadd_rn(a, part[(long long)ch * sh.dim + e]);
     tt = __dadd_rn(tt, tpart[(long long)ch * sh.N + m]);
   }

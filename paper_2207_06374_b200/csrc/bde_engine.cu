@@ -310,8 +310,7 @@ static int run_obj(Engine* E, const int* act, int nreq, bool any_wout, cudaStrea
                                                                                   : launch_grad<true, 32>(P, nreq, KS, st);
   else e = ib == 64 ? launch_grad<false, 64>(P, nreq, KS, st) : launch_grad<false, 32>(P, nreq, KS, st);
   BCHK(e);
-  // one chunk group: the contraction folded the chunk partials (CAS order) into slot 0
-  bde_finalize<<<dim3((unsigned)((sh.dim + 255) / 256), nreq), 256, 0, st>>>(P, KS == 1 ? 1 : sh.K);
+  bde_finalize<<<dim3((unsigned)((sh.dim + 255) / 256), nreq), 256, 0, st>>>(P);
   g_launches += 6;
   if (any_wout) {
     bde_wout<<<dim3(256, nreq), 256, 0, st>>>(P);

@@ -172,7 +172,7 @@ def test_gradient_chunk_groups_same_bits(ctx, field, d, N):
     for B in (1, 3, 40):
         pts = np.repeat(x[None], B, axis=0)
         F, s, g, _, zc = ctx.eval_batch(field, d, N, pts, 1e-2)
-        for b in (0, B - 1):
+        for b in range(B):  # every copy, every launch: a race in the producer / consumer pipeline would show here
             assert zc[b] == -1 and bits(F[b]) == bits(Fo)
             assert np.array_equal(bits(g[b]), bits(go))
 
