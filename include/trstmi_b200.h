@@ -189,6 +189,10 @@ int trstmi_default_schedule(int64_t N, double eps_target, double* out, int cap);
  * the stage-boundary rescue. Host-only (Box-Muller uses libm). */
 int trstmi_random_frames(int field, int64_t d, int64_t N, uint64_t seed, int64_t first, int64_t count,
                          double* frames, uint64_t* rng_state);
+/* random_frame (solver.hpp:87-98) from the plain generator SplitMix64(rng_seed)
+ * (no child-seed mixing): the start of alternating_projection(d, N, cfg, rng),
+ * baseline.hpp:84, and of the reference's tests that seed a generator directly. */
+int trstmi_random_frame_seeded(int field, int64_t d, int64_t N, uint64_t rng_seed, double* frame);
 
 /* ---- objective / gradient (eval_objective at B points) ----
  * pts: B x dim.  delta: B values.  squared: 1 (solver mode) or 0 (magnitude).
@@ -293,6 +297,22 @@ int trstmi_distortion_mc(int64_t d, int64_t N, const double* codebook, uint64_t 
                          double* estimate, double* std_error);
 /* check_tight's deviation (analysis.hpp:76-84): max |(Phi Phi*)(r,s) - (N/d) I| */
 int trstmi_frame_operator_deviation(int field, int64_t d, int64_t N, const double* frame, double* deviation);
+
+/* ---- alternating-projection baseline (csrc/altproj.cu).
+ * alternating_projection (baseline.hpp:68-167) for `restarts` complex d x N start
+ * frames (restarts x 2dN doubles, interleaved column-major; restart i of
+ * solve_altproj, baseline.hpp:172-199, starts from random_frame of the child
+ * generator mix_seed(seed, i): trstmi_random_frames(TRSTMI_COMPLEX, ...)).
+ * One CTA per restart.  mu_target 0 -> max(welch_bound(d, N), 1e-12); tol =
+ * AltProjConfig::tol (max-entry change of the Gram).  Outputs per restart: the
+ * result frame (the converged iterate, else the best seen), its coherence,
+ * iterations (> 0: converged after that many, < 0: best of -iterations, the
+ * sign convention of StageRecord::outer_iterations, baseline.hpp:156) and the
+ * Jacobi sweeps spent (nullable).  INVALID_ARG where the reference throws
+ * std::invalid_argument (d > N, max_iters < 1, mu_target >= 1) and for N > 256. */
+int trstmi_altproj_batch(int64_t d, int64_t N, int32_t max_iters, double mu_target, double tol, int64_t restarts,
+                         const double* starts, double* frames, double* coherence, int32_t* iterations,
+                         int32_t* sweeps);
 
 #ifdef __cplusplus
 }

@@ -7,6 +7,7 @@
 
 #include "../include/trstmi_b200.h"
 #include "cas_oracle.hpp"
+#include "altproj_oracle.hpp"
 
 using namespace orc;
 
@@ -345,6 +346,28 @@ double orc_time_solve_batch(const trstmi_cfg* c, int lanes, std::int64_t trials,
   *outer = o;
   *evals = e;
   return sec;
+}
+
+// alternating_projection (baseline.hpp:68-167) for `restarts` start frames (restarts x 2dN doubles, each the
+// random_frame of its own child generator): the checker of trstmi_altproj_batch.  iterations[r] > 0: converged
+// after that many iterations, < 0: the best iterate after -iterations[r] (StageRecord::outer_iterations).
+int orc_altproj_batch(std::int64_t d, std::int64_t N, int max_iters, double mu_target, double tol, std::int64_t restarts,
+                      const double* starts, double* frames, double* coherences, std::int32_t* iterations,
+                      std::int32_t* sweeps) {
+  if (d < 1 || N < 1 || d > N || max_iters < 1) return TRSTMI_ERR_INVALID_ARG;
+  AltProjCfg cfg;
+  cfg.max_iters = max_iters;
+  cfg.mu_target = mu_target;
+  cfg.tol = tol;
+  const std::int64_t dim = 2 * d * N;
+  for (std::int64_t r = 0; r < restarts; ++r) {
+    const AltProjOut o = altproj_run((int)d, (int)N, cfg, starts + r * dim);
+    std::memcpy(frames + r * dim, o.frame.data(), dim * sizeof(double));
+    coherences[r] = o.coherence;
+    iterations[r] = o.iterations;
+    if (sweeps) sweeps[r] = o.jacobi_sweeps;
+  }
+  return TRSTMI_OK;
 }
 
 }  // extern "C"

@@ -88,6 +88,8 @@ def load_library():
     lib.trstmi_comm_init.argtypes = [vp, c_int, c_int, vp]
     lib.trstmi_best_of_ranks.argtypes = [vp, c_i64, c_dbl, c_i64, vp, vp, vp, vp, vp]
     lib.trstmi_solve_sharded.argtypes = [vp, vp, c_i64, ctypes.c_uint64, vp, vp, vp, vp, vp, vp]
+    lib.trstmi_random_frame_seeded.argtypes = [c_int, c_i64, c_i64, ctypes.c_uint64, vp]
+    lib.trstmi_altproj_batch.argtypes = [c_i64, c_i64, ctypes.c_int32, c_dbl, c_dbl, c_i64, vp, vp, vp, vp, vp]
     lib.trstmi_launch_count.restype = ctypes.c_longlong
     lib.trstmi_measure_dfma_peak.argtypes = [vp, c_int, vp]
     _lib = lib

@@ -81,7 +81,7 @@ def build(verbose=False, force=False, jobs=None):
     for cplx, s, g in INSTANCES:
         o = os.path.join(BUILD, "inst_%s_%d_%s.o" % ("c" if cplx else "r", s, "g" if g else "r"))
         add(os.path.join(CSRC, "instantiate.cu"), o, ["-DINST_CPLX=%d" % cplx, "-DINST_S=%d" % s, "-DINST_GS=%d" % g])
-    for src in ("trstmi_capi.cu", "large_engine.cu", "analysis.cu", "sharding.cu", "bde_engine.cu"):
+    for src in ("trstmi_capi.cu", "large_engine.cu", "analysis.cu", "sharding.cu", "bde_engine.cu", "altproj.cu"):
         add(os.path.join(CSRC, src), os.path.join(BUILD, src.replace(".cu", ".o")), [])
     with cf.ThreadPoolExecutor(jobs) as ex:
         for log in ex.map(lambda c: _run([NVCC] + c), tasks):

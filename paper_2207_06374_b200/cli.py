@@ -9,8 +9,8 @@ the reference's tools/main.cpp (/root/reference/proj/tools/main.cpp):
   distortion --in FRAME [--samples N] [--seed S]          cmd_distortion main.cpp:269-279
 
 Same output lines, CSV columns and JSON keys as the reference.  --threads is
-accepted for compatibility (restarts run as a GPU batch).  The altproj method
-is outside this build's scope and exits with status 2.
+accepted for compatibility (restarts run as a GPU batch).  --method altproj
+runs the alternating-projection baseline on the GPU (baseline.py, csrc/altproj.cu).
 
   python -m paper_2207_06374_b200.cli solve --d 2 --N 4 --restarts 20 --seed 7 --out r.json
 """
@@ -45,9 +45,16 @@ def _cfg(args, N):
 
 
 def run_method(args, N):
-    """main.cpp:60-83 (trstmi only)."""
+    """main.cpp:60-83."""
+    if args.method == "altproj":
+        if args.field == "real":
+            raise NotImplementedError("method 'altproj' works on complex frames (the reference has no real mode)")
+        from . import baseline
+        cfg = baseline.AltProjConfig()
+        result = baseline.solve_altproj(args.d, N, cfg, args.restarts, args.seed)
+        return result, baseline.altproj_config_to_json(args.d, N, cfg, args.restarts, args.seed)
     if args.method != "trstmi":
-        raise NotImplementedError("method '%s' is not part of this build (trstmi only)" % args.method)
+        raise NotImplementedError("method '%s' is not part of this build (trstmi or altproj)" % args.method)
     cfg = _cfg(args, N)
     result = rec.solve(cfg, restarts=args.restarts, seed=args.seed)
     return result, rec.solver_config_to_json(cfg, args.restarts, args.seed)

@@ -40,10 +40,18 @@ struct AnnealArgs {
   trstmi_outer_out* oout;   // nullable: trials x record_cap
 };
 
+// extra doubles of the dual layout: phiS grows to a second phiC (column stride gs_col_stride(L)), a second alpha,
+// one double of alignment
+__host__ __device__ inline long long dual_smem_doubles(const Prob& P) {
+  return (P.gs && P.dual) ? (long long)(gs_col_stride(P.L) - P.L) * P.N + P.N + 1 : 0;
+}
+
+
 // doubles of shared memory the anneal kernel needs for a shape
 __host__ __device__ inline long long smem_doubles(const Prob& P, int S, bool cplx, int nvec) {
   const int W = S / 32;
-  return (long long)P.L * P.N + P.N + pair_smem_doubles(P, cplx) + 1 + 2LL * 4 * W + 4 + (long long)nvec * P.dim + W;
+  return (long long)P.L * P.N + P.N + pair_smem_doubles(P, cplx) + 1 + 2LL * 4 * W + 4 + (long long)nvec * P.dim + W +
+         dual_smem_doubles(P);
 }
 __host__ __device__ inline long long anneal_smem_doubles(const Prob& P, int S, bool cplx) {
   return smem_doubles(P, S, cplx, 9);
@@ -64,10 +72,16 @@ __device__ __forceinline__ void carve(const Prob& P, int S, double* base, Smem& 
     sm.GRI = sm.phiC = nullptr;
     sm.fk = nullptr;
   }
+  if (P.gs && P.dual) p += (p - base) & 1;  // 16-byte aligned: phiS doubles as the second phiC
   sm.phiS = p;
-  p += P.L * P.N;
+  p += (P.gs && P.dual) ? gs_col_stride(P.L) * P.N : P.L * P.N;
   sm.alpha = p;
   p += P.N;
+  sm.alpha2 = nullptr;
+  if (P.gs && P.dual) {
+    sm.alpha2 = p;
+    p += P.N;
+  }
   sm.U = p;
   p += P.gs ? P.np : P.n;
   sm.part = p;
@@ -130,6 +144,9 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
     __syncthreads();
     if (li >= A.n_list) break;
     const int trial = A.list ? A.list[li] : li;
+#ifdef TRSTMI_PHASE_TIMERS
+    const long long t_trial_ = clock64();
+#endif
     const int k0 = A.start_stage ? A.start_stage[trial] : 0;
     trstmi_trial_out* TO = A.tout + trial;
     long long outer = 0, evals = 0, hvps = 0, nrec = 0;
@@ -220,8 +237,13 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
               const double h = kFdBaseStep * (1.0 + xnorm) / fmax(dn, 1e-300);
               __syncthreads();
               evals += 2;
-              const int zp = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, dv, h, delta, sm, rbuf, bd, nullptr, nullptr, nullptr);
-              if (zp < 0) {
+              int zp = INT_MAX - 1;
+              if constexpr (GS) {  // both points in one pass (bit-identical; falls through when a column vanishes)
+                if (P.dual) zp = hvp_cta_gs<CPLX, DMAX, EXACT, S>(P, x, dv, h, delta, sm, rbuf, bd);
+              }
+              if (zp == -1) {
+                // bd = (g(x + h d) - g(x - h d)) / (2h) already formed
+              } else if ((zp = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, dv, h, delta, sm, rbuf, bd, nullptr, nullptr, nullptr)) < 0) {
                 const int zm = eval_any<CPLX, DMAX, EXACT, S, GS>(P, x, dv, -h, delta, sm, rbuf, gt, nullptr, nullptr, nullptr);
                 if (zm < 0) {
                   const double h2 = 2.0 * h;
@@ -281,12 +303,17 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
               break;
             }
             const double alpha = rr / dbd;
-            double zn = 0.0;
+            // ||z + alpha d||^2 and, speculatively, ||r + alpha B d||^2 (needed only when the step stays inside) in
+            // one CTA reduction: each sum keeps its own CAS order
+            double znrn[2] = {0.0, 0.0};
             for (int i = tid; i < dim; i += S) {
               const double t = zs[i] + alpha * dv[i];
-              zn = fma(t, t, zn);
+              znrn[0] = fma(t, t, znrn[0]);
+              const double rt = r[i] + alpha * bd[i];
+              znrn[1] = fma(rt, rt, znrn[1]);
             }
-            if (sqrt(block_sum1<S>(zn, sm.red, rbuf)) >= radius) {
+            block_sum<S, 2>(znrn, sm.red, rbuf);
+            if (sqrt(znrn[0]) >= radius) {
               double br[3] = {dot_partial<S>(dv, dv, dim), dot_partial<S>(zs, dv, dim), dot_partial<S>(zs, zs, dim)};
               block_sum<S, 3>(br, sm.red, rbuf);
               const double a = br[0], b = 2.0 * br[1], c = br[2] - radius * radius;
@@ -311,13 +338,11 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
               break;
             }
             model += alpha * rd + 0.5 * alpha * alpha * dbd;
-            double rn = 0.0;
             for (int i = tid; i < dim; i += S) {
               zs[i] = zs[i] + alpha * dv[i];
               r[i] = r[i] + alpha * bd[i];
-              rn = fma(r[i], r[i], rn);
             }
-            const double rr_next = block_sum1<S>(rn, sm.red, rbuf);
+            const double rr_next = znrn[1];
             cg_iters = j + 1;
             if (sqrt(rr_next) < eps_k) {
               cg_exit = TRSTMI_CG_SMALL_RESIDUAL;
@@ -456,6 +481,9 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) anneal_small_kern
       o.records = nrec;
       *TO = o;
     }
+#ifdef TRSTMI_PHASE_TIMERS
+    if (tid == 0) atomicAdd(&g_phase_cycles[7], (unsigned long long)(clock64() - t_trial_));
+#endif
     __syncthreads();
   }
 }

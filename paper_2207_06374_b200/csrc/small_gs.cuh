@@ -32,15 +32,43 @@
 #ifndef TRSTMI_GS_UNROLL
 #define TRSTMI_GS_UNROLL 4
 #endif
+#ifndef TRSTMI_GS_GRAM_COLS
+#define TRSTMI_GS_GRAM_COLS 1  // Gram sweep by (row chunk, column) units; 0: lane-strided pair-table sweep
+#endif
 
 namespace trstmi_dev {
 
 constexpr int kGsUnroll = TRSTMI_GS_UNROLL;  // k steps of the branch-free gradient loop in flight
+constexpr int kGsDualElems = 4;              // gradient elements per thread the fused central difference keeps in registers
 
 // Slot tables and zeroed pair arrays.  Once per kernel; ends with a barrier.
 template <int S, bool CPLX>
-__device__ __forceinline__ void build_gs_tables(const Prob& P, const Smem& sm) {
+__device__ __forceinline__ void build_gs_tables(const Prob& P, Smem& sm) {
   constexpr int C = CPLX ? 2 : 1;
+  {
+    // Gram sweep units (gs_gram_sweep): rows in chunks of c, chunk ch = rows [c ch, c ch + c) against every column
+    // k > c ch; c is the smallest length whose unit count fits the CTA, so each thread owns at most one unit.
+    // (Two columns per thread — half the row loads per pair — measured slower: profiles/r2_c2_session5.md.)
+    const int R = P.N - 1;
+    int c = 1;
+    for (;; ++c) {
+      const int nch = (R + c - 1) / c;
+      if (nch * R - c * (nch * (nch - 1) / 2) <= S) break;
+    }
+    int u = threadIdx.x, ch = 0;
+    while (c * ch < R && u >= R - c * ch) {
+      u -= R - c * ch;
+      ++ch;
+    }
+    if (c * ch < R) {
+      sm.gk = c * ch + 1 + u;
+      sm.gj0 = c * ch;
+      sm.gj1 = min(c * ch + c, sm.gk);
+    } else {
+      sm.gk = -1;
+      sm.gj0 = sm.gj1 = 0;
+    }
+  }
   for (int i = threadIdx.x; i < P.np; i += S) {
     sm.U[i] = 0.0;
 #pragma unroll
@@ -107,63 +135,85 @@ __device__ __forceinline__ void gram_regs(const double* a, const double* b, int 
   }
 }
 
-template <bool CPLX, int DMAX, bool EXACT, int S, bool SQ = true>
-__device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const double* __restrict__ dir, double sc,
-                           double delta, const Smem& sm, int& rbuf, double* __restrict__ gout, double* F_out,
-                           double* s_out, double* __restrict__ wout) {
+// ---- the phases of one evaluation, shared by eval_cta_gs and hvp_cta_gs.  phiC / alpha are parameters so the two
+// points of a central difference can keep their normalised columns side by side.
+
+// phase 1, one column: alpha_j = ||p_j||, phi_j = p_j / alpha_j (smoothing.hpp:95-102), p = x + sc dir.
+// Returns true when the column is (numerically) zero; phi_j is then left unwritten.
+template <bool CPLX, int DMAX, bool EXACT>
+__device__ __forceinline__ bool gs_norm_col(const Prob& P, const double* __restrict__ x, const double* __restrict__ dir,
+                                            double sc, int j, double* __restrict__ phiC, double* __restrict__ alpha,
+                                            int LP) {
   constexpr int C = CPLX ? 2 : 1;
   constexpr int LM = C * DMAX;
   const int d = EXACT ? DMAX : P.d;
-  const int N = P.N, L = P.L, n = P.n;
-  const int LP = EXACT ? gs_col_stride(LM) : gs_col_stride(L);
-  const int tid = threadIdx.x;
-  const int NW = mask_words(N);
+  const int L = P.L;
+  double col[LM];
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < LM; ++q) {
+    if (q < C * d) {
+      const double xv = x[j * L + q];
+      const double pv = (sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(sc, dir[j * L + q]));
+      col[q] = pv;
+      acc = fma(pv, pv, acc);
+    }
+  }
+  const double a = sqrt(acc);
+  alpha[j] = a;
+  if (a < kZeroColumnTol) return true;
+  const double ya = __drcp_rn(a);
+#pragma unroll
+  for (int q = 0; q < LM; ++q)
+    if (q < C * d) phiC[j * LP + q] = div_rn(col[q], a, ya);
+  return false;
+}
+
+// phase 2: Gram upper triangle (smoothing.hpp:104-118): slot <- (re, im), U <- x_p; returns the thread's max x_p
+// ((xv > smax) skips NaNs like the reference's std::max).
+template <bool CPLX, int DMAX, bool EXACT, int S, bool SQ>
+__device__ __forceinline__ double gs_gram_sweep(const Prob& P, const Smem& sm, const double* __restrict__ phiC, int LP) {
+  constexpr int C = CPLX ? 2 : 1;
+  constexpr int LM = C * DMAX;
+  const int d = EXACT ? DMAX : P.d;
+  const int n = P.n;
   double* __restrict__ U = sm.U;
   double* __restrict__ GRI = sm.GRI;
-  double* __restrict__ phiC = sm.phiC;
   const unsigned* __restrict__ tab = sm.jk;
-  PHASE_START;
-
-  // ---- phase 1: column norms, normalisation (smoothing.hpp:95-102)
-  int zc = INT_MAX;
-  for (int j = tid; j < N; j += S) {
-    double col[LM];
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < LM; ++q) {
-      if (q < C * d) {
-        const double xv = x[j * L + q];
-        const double pv = (sc == 0.0) ? xv : __dadd_rn(xv, __dmul_rn(sc, dir[j * L + q]));
-        col[q] = pv;
-        acc = fma(pv, pv, acc);
+  double smax = -__longlong_as_double(0x7ff0000000000000LL);
+#if TRSTMI_GS_GRAM_COLS
+  // Thread = (row chunk, column k): column k stays in registers, the rows j of the chunk arrive as warp-wide
+  // loads of one address (every lane of a chunk is at the same j), and the stores of a warp go to consecutive
+  // slots f(j) + k — two thirds of the shared-memory traffic of a pair-table sweep, and no table.
+  if (sm.gk >= 0) {
+    const int k = sm.gk;
+    const int* __restrict__ fk = sm.fk;
+    double b[LM];
+    load_col<LM, EXACT>(phiC + k * LP, b, C * d);
+#pragma unroll 4
+    for (int j = sm.gj0; j < sm.gj1; ++j) {
+      double a[LM];
+      load_col<LM, EXACT>(phiC + j * LP, a, C * d);
+      double re, im;
+      gram_regs<CPLX, DMAX, EXACT>(a, b, d, re, im);
+      const double uu = CPLX ? __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im)) : __dmul_rn(re, re);
+      double xv = uu;
+      if constexpr (!SQ) xv = sqrt(uu);
+      const int ph = fk[j] + k;
+      U[ph] = xv;
+      if constexpr (CPLX) {
+        *reinterpret_cast<double2*>(GRI + 2 * ph) = make_double2(re, im);
+      } else {
+        GRI[ph] = re;
       }
-    }
-    const double a = sqrt(acc);
-    sm.alpha[j] = a;
-    if (a < kZeroColumnTol) {
-      zc = min(zc, j);
-    } else {
-      const double ya = __drcp_rn(a);
-#pragma unroll
-      for (int q = 0; q < LM; ++q)
-        if (q < C * d) phiC[j * LP + q] = div_rn(col[q], a, ya);
+      smax = xv > smax ? xv : smax;
     }
   }
-  zc = block_min_int<S>(zc, sm.ired, rbuf);  // also publishes phiC / alpha
-  PHASE_MARK(0);
-  if (zc != INT_MAX) {
-    for (int i = tid; i < P.dim; i += S) gout[i] = 0.0;
-    if (F_out) *F_out = __longlong_as_double(0x7ff0000000000000LL);
-    if (s_out) *s_out = 0.0;
-    __syncthreads();
-    return zc;
-  }
-
-  // ---- phase 2: Gram upper triangle (smoothing.hpp:104-118): slot <- (re,
-  // im), U <- x_p; s = max x_p (fmax skips NaNs like the reference's std::max)
-  double smax = -__longlong_as_double(0x7ff0000000000000LL);  // (xv > smax) skips NaNs like std::max
+  (void)n;
+  (void)tab;
+#else
 #pragma unroll 2
-  for (int p = tid; p < n; p += S) {
+  for (int p = threadIdx.x; p < n; p += S) {
     const unsigned t = tab[p];
     const int ph = (int)(t & 0xffffu);
     const int j = (int)((t >> 16) & 0xffu), k = (int)(t >> 24);
@@ -183,16 +233,28 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
     }
     smax = xv > smax ? xv : smax;
   }
+#endif
   if (sm.scal[3] != 0.0)
-    for (int i = tid; i < N * NW; i += S) sm.mask[i] = 0u;  // published by block_max's barrier
-  const double s = block_max<S>(smax, sm.red, rbuf);
-  PHASE_MARK(1);
+    for (int i = threadIdx.x; i < P.N * mask_words(P.N); i += S) sm.mask[i] = 0u;  // published by block_max's barrier
+  return smax;
+}
 
-  // ---- phase 3a: w = exp((x - s)/delta) (smoothing.hpp:118-124); 0 where
-  // (x - s) < cut (exactly where exp underflows to 0); z lane partials in CAS
-  // order.  When the previous evaluation of this CTA was sparse, also the
-  // nonzero pattern (mask words cleared in phase 2); any choice of gradient
-  // loop gives the same bits, so a stale prediction only costs time.
+struct GsZ {
+  double z, yz;
+  bool sparse, use_mask, chkdiv;
+};
+
+// phase 3a: w = exp((x - s)/delta) (smoothing.hpp:118-124); 0 where (x - s) < cut (exactly where exp underflows
+// to 0); z lane partials in CAS order, then the CTA sum.  When the previous evaluation of this CTA was sparse, also
+// the nonzero pattern (mask words cleared in phase 2); any choice of gradient loop gives the same bits, so a stale
+// prediction only costs time.
+template <int S>
+__device__ __forceinline__ GsZ gs_exp_z(const Prob& P, const Smem& sm, double s, double delta, int& rbuf) {
+  const int n = P.n;
+  const int tid = threadIdx.x;
+  const int NW = mask_words(P.N);
+  double* __restrict__ U = sm.U;
+  const unsigned* __restrict__ tab = sm.jk;
   const bool build_mask = sm.scal[3] != 0.0;
   const double cut = __dmul_rn(kUnderflowCut, delta);
   const double ydelta = __drcp_rn(delta);
@@ -265,29 +327,34 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
   }
   double zz[3] = {zl, (double)nnz, (double)tiny};
   block_sum<S, 3>(zz, sm.red, rbuf);
-  PHASE_MARK(2);
-  const double z = zz[0];
-  const bool sparse = zz[1] * 4.0 < (double)n;
-  const bool use_mask = build_mask && sparse;
-  const bool chkdiv = zz[2] != 0.0;
-  const double yz = __drcp_rn(z);
-  // c_p = w_p / z (smoothing.hpp:125), computed where it is used (phase 4);
-  // the softmax weights are written only when asked for (batch eval API)
-  if (wout) {
-    for (int p = tid; p < n; p += S) {
-      const double w = U[tab[p] & 0xffffu];
-      wout[p] = (w > 0.0 && w < 0x1.0p-900) ? ieee_div(w, z) : div_fast(w, z, yz);
-    }
-  }
-  PHASE_MARK(3);
+  GsZ r;
+  r.z = zz[0];
+  r.sparse = zz[1] * 4.0 < (double)n;
+  r.use_mask = build_mask && r.sparse;
+  r.chkdiv = zz[2] != 0.0;
+  r.yz = __drcp_rn(r.z);
+  return r;
+}
 
-  // ---- phase 4: gradient (smoothing.hpp:130-160), CAS chunked order.
-  // Thread (chunk ch, column m), ascending k in [ch*N/K, (ch+1)*N/K):
-  // slot(k, m) = k < m ? f(k) + m : f(m) + k (k == m: the zero slot before
-  // row m), t += c u, acc += phi_k * (c G(k,m)) with c Im G(k,m) = +-slot.im.
+// phase 4: gradient (smoothing.hpp:130-160), CAS chunked order.
+// Thread (chunk ch, column m), ascending k in [ch*N/K, (ch+1)*N/K):
+// slot(k, m) = k < m ? f(k) + m : f(m) + k (k == m: the zero slot before
+// row m), t += c u, acc += phi_k * (c G(k,m)) with c Im G(k,m) = +-slot.im;
+// c_p = w_p / z (smoothing.hpp:125) is computed where it is used.  Chunk partials -> sm.part (no barrier here).
+template <bool CPLX, int DMAX, bool EXACT, int S, bool SQ>
+__device__ __forceinline__ void gs_grad_loop(const Prob& P, const Smem& sm, const double* __restrict__ phiC, int LP,
+                                             const GsZ& Z) {
+  constexpr int C = CPLX ? 2 : 1;
+  constexpr int LM = C * DMAX;
+  const int d = EXACT ? DMAX : P.d;
+  const int N = P.N, L = P.L;
+  const int NW = mask_words(N);
+  const double* __restrict__ U = sm.U;
+  const double* __restrict__ GRI = sm.GRI;
+  const double z = Z.z, yz = Z.yz;
   const int K = P.K;
   const int* __restrict__ fk = sm.fk;
-  for (int unit = tid; unit < K * N; unit += S) {
+  for (int unit = threadIdx.x; unit < K * N; unit += S) {
     const int ch = unit / N;
     const int m = unit - ch * N;
     const int k_lo = (ch * N) / K, k_hi = ((ch + 1) * N) / K;
@@ -334,7 +401,7 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
           if (i < d) acc[i] = fma(pk[i], cr, acc[i]);
       }
     };
-    if (use_mask) {
+    if (Z.use_mask) {
       const unsigned* mrow = sm.mask + m * NW;
       for (int wi = k_lo >> 5; wi <= ((k_hi - 1) >> 5); ++wi) {
         unsigned wd = mrow[wi];
@@ -348,7 +415,7 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
           term(k, lower ? fk[k] + m : fm + k, lower, BoolTag<true>{});
         }
       }
-    } else if (chkdiv) {
+    } else if (Z.chkdiv) {
 #pragma unroll 2
       for (int k = k_lo; k < k_hi; ++k) {
         const bool lower = k < m;
@@ -367,26 +434,153 @@ __device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const do
       if (q < C * d) pp[q] = acc[q];
     pp[L] = tp;
   }
+}
+
+// phase 5, one output element mq = m L + q: chunk partials left to right, ((acc - t phi)/alpha) * 2.
+__device__ __forceinline__ double gs_combine_elem(const Prob& P, const Smem& sm, const double* __restrict__ phiC,
+                                                  const double* __restrict__ alpha, int LP, int mq) {
+  const int N = P.N, L = P.L, K = P.K;
+  const int m = mq / L;
+  const int q = mq - m * L;
+  double a = 0.0, t = 0.0;
+  for (int ch = 0; ch < K; ++ch) {
+    const double* pp = sm.part + (long long)(ch * N + m) * (L + 1);
+    a = ch == 0 ? pp[q] : __dadd_rn(a, pp[q]);
+    t = ch == 0 ? pp[L] : __dadd_rn(t, pp[L]);
+  }
+  const double am = alpha[m];
+  return __dmul_rn(div_rn(__dsub_rn(a, __dmul_rn(t, phiC[m * LP + q])), am, __drcp_rn(am)), 2.0);
+}
+
+template <bool CPLX, int DMAX, bool EXACT, int S, bool SQ = true>
+__device__ int eval_cta_gs(const Prob& P, const double* __restrict__ x, const double* __restrict__ dir, double sc,
+                           double delta, const Smem& sm, int& rbuf, double* __restrict__ gout, double* F_out,
+                           double* s_out, double* __restrict__ wout) {
+  constexpr int C = CPLX ? 2 : 1;
+  constexpr int LM = C * DMAX;
+  const int N = P.N, L = P.L, n = P.n;
+  const int LP = EXACT ? gs_col_stride(LM) : gs_col_stride(L);
+  const int tid = threadIdx.x;
+  double* __restrict__ phiC = sm.phiC;
+  PHASE_START;
+
+  // ---- phase 1: column norms, normalisation (smoothing.hpp:95-102)
+  int zc = INT_MAX;
+  for (int j = tid; j < N; j += S)
+    if (gs_norm_col<CPLX, DMAX, EXACT>(P, x, dir, sc, j, phiC, sm.alpha, LP)) zc = min(zc, j);
+  zc = block_min_int<S>(zc, sm.ired, rbuf);  // also publishes phiC / alpha
+  PHASE_MARK(0);
+  if (zc != INT_MAX) {
+    for (int i = tid; i < P.dim; i += S) gout[i] = 0.0;
+    if (F_out) *F_out = __longlong_as_double(0x7ff0000000000000LL);
+    if (s_out) *s_out = 0.0;
+    __syncthreads();
+    return zc;
+  }
+
+  // ---- phase 2
+  const double smax = gs_gram_sweep<CPLX, DMAX, EXACT, S, SQ>(P, sm, phiC, LP);
+  const double s = block_max<S>(smax, sm.red, rbuf);
+  PHASE_MARK(1);
+
+  // ---- phase 3a
+  const GsZ Z = gs_exp_z<S>(P, sm, s, delta, rbuf);
+  PHASE_MARK(2);
+  // the softmax weights are written only when asked for (batch eval API)
+  if (wout) {
+    for (int p = tid; p < n; p += S) {
+      const double w = sm.U[sm.jk[p] & 0xffffu];
+      wout[p] = (w > 0.0 && w < 0x1.0p-900) ? ieee_div(w, Z.z) : div_fast(w, Z.z, Z.yz);
+    }
+  }
+  PHASE_MARK(3);
+
+  // ---- phase 4
+  gs_grad_loop<CPLX, DMAX, EXACT, S, SQ>(P, sm, phiC, LP, Z);
   if (tid == S - 1) {  // off the critical path when K*N < S (this thread has no unit)
-    if (F_out) *F_out = __dadd_rn(s, __dmul_rn(delta, cas_log(z)));
+    if (F_out) *F_out = __dadd_rn(s, __dmul_rn(delta, cas_log(Z.z)));
     if (s_out) *s_out = s;
-    sm.scal[3] = sparse ? 1.0 : 0.0;  // mask prediction for the next evaluation
+    sm.scal[3] = Z.sparse ? 1.0 : 0.0;  // mask prediction for the next evaluation
   }
   __syncthreads();
   PHASE_MARK(4);
-  for (int mq = tid; mq < N * L; mq += S) {
-    const int m = mq / L;
-    const int q = mq - m * L;
-    double a = 0.0, t = 0.0;
-    for (int ch = 0; ch < K; ++ch) {
-      const double* pp = sm.part + (long long)(ch * N + m) * (L + 1);
-      a = ch == 0 ? pp[q] : __dadd_rn(a, pp[q]);
-      t = ch == 0 ? pp[L] : __dadd_rn(t, pp[L]);
-    }
-    const double am = sm.alpha[m];
-    gout[m * L + q] = __dmul_rn(div_rn(__dsub_rn(a, __dmul_rn(t, phiC[m * LP + q])), am, __drcp_rn(am)), 2.0);
-  }
+  for (int mq = tid; mq < N * L; mq += S) gout[mq] = gs_combine_elem(P, sm, phiC, sm.alpha, LP, mq);
   __syncthreads();
+  PHASE_MARK(5);
+  return -1;
+}
+
+// Central finite difference (g(x + h dir) - g(x - h dir)) / (2h) (smoothing.hpp:167-181, solver.hpp:118-137) as
+// ONE pass over the phases of the two evaluations: both points are normalised in one phase (the + point into
+// phiC / alpha, the - point into phiS / alpha2 — the dual layout), the + point's combine runs inside the - point's
+// Gram phase (the latency chains of one hide behind the sweep of the other), and the - point's combine forms the
+// quotient directly.  Every value is computed by the operations of eval_cta_gs in the same order, so bd is
+// bit-identical to two eval_cta_gs calls followed by (g+ - g-) / (2h).  Returns -1, or INT_MAX - 1 when either
+// point has a zero column: nothing but scratch has been written then and the caller takes the step-by-step path.
+// Needs P.dual.  No barrier at the end: each thread has written the bd elements mq = tid, tid + S, ... it owns.
+template <bool CPLX, int DMAX, bool EXACT, int S>
+__device__ int hvp_cta_gs(const Prob& P, const double* __restrict__ x, const double* __restrict__ dir, double h,
+                          double delta, const Smem& sm, int& rbuf, double* __restrict__ bd) {
+  constexpr int C = CPLX ? 2 : 1;
+  constexpr int LM = C * DMAX;
+  const int N = P.N, L = P.L;
+  const int LP = EXACT ? gs_col_stride(LM) : gs_col_stride(L);
+  const int tid = threadIdx.x;
+  double* __restrict__ phiA = sm.phiC;
+  double* __restrict__ phiB = sm.phiS;
+  PHASE_START;
+
+  // ---- phase 1 of both points: warps [0, NR/32) take the + point, the next NR/32 warps the - point
+  const int NR = (N + 31) & ~31;
+  int zc = INT_MAX;
+  for (int u = tid; u < 2 * NR; u += S) {
+    const int side = u >= NR;
+    const int j = u - side * NR;
+    if (j < N) {
+      const bool zero = side ? gs_norm_col<CPLX, DMAX, EXACT>(P, x, dir, -h, j, phiB, sm.alpha2, LP)
+                             : gs_norm_col<CPLX, DMAX, EXACT>(P, x, dir, h, j, phiA, sm.alpha, LP);
+      if (zero) zc = min(zc, j);
+    }
+  }
+  zc = block_min_int<S>(zc, sm.ired, rbuf);
+  PHASE_MARK(0);
+  if (zc != INT_MAX) return INT_MAX - 1;
+
+  // ---- + point: phases 2-4
+  double s = block_max<S>(gs_gram_sweep<CPLX, DMAX, EXACT, S, true>(P, sm, phiA, LP), sm.red, rbuf);
+  PHASE_MARK(1);
+  GsZ Z = gs_exp_z<S>(P, sm, s, delta, rbuf);
+  PHASE_MARK(2);
+  gs_grad_loop<CPLX, DMAX, EXACT, S, true>(P, sm, phiA, LP, Z);
+  if (tid == S - 1) sm.scal[3] = Z.sparse ? 1.0 : 0.0;
+  __syncthreads();
+  PHASE_MARK(4);
+
+  // ---- + point: combine (reads part, phiA, alpha) inside the - point's Gram phase (writes the pair slots, reads phiB)
+  double gp[kGsDualElems];  // the dual layout is only chosen when dim <= kGsDualElems * S
+#pragma unroll
+  for (int e = 0; e < kGsDualElems; ++e) {
+    const int mq = tid + e * S;
+    gp[e] = mq < N * L ? gs_combine_elem(P, sm, phiA, sm.alpha, LP, mq) : 0.0;
+  }
+  s = block_max<S>(gs_gram_sweep<CPLX, DMAX, EXACT, S, true>(P, sm, phiB, LP), sm.red, rbuf);
+  PHASE_MARK(1);
+  Z = gs_exp_z<S>(P, sm, s, delta, rbuf);
+  PHASE_MARK(2);
+  gs_grad_loop<CPLX, DMAX, EXACT, S, true>(P, sm, phiB, LP, Z);
+  if (tid == S - 1) sm.scal[3] = Z.sparse ? 1.0 : 0.0;
+  __syncthreads();
+  PHASE_MARK(4);
+
+  // ---- - point: combine, and the quotient (solver.hpp:127)
+  {
+    const double h2 = 2.0 * h;
+#pragma unroll
+    for (int e = 0; e < kGsDualElems; ++e) {
+      const int mq = tid + e * S;
+      if (mq < N * L) bd[mq] = (gp[e] - gs_combine_elem(P, sm, phiB, sm.alpha2, LP, mq)) / h2;
+    }
+  }
   PHASE_MARK(5);
   return -1;
 }
@@ -403,7 +597,7 @@ __device__ __forceinline__ int eval_any(const Prob& P, const double* __restrict_
 }
 
 template <int S, bool CPLX, bool GS>
-__device__ __forceinline__ void build_tables(const Prob& P, const Smem& sm) {
+__device__ __forceinline__ void build_tables(const Prob& P, Smem& sm) {
   if constexpr (GS)
     build_gs_tables<S, CPLX>(P, sm);
   else

@@ -61,6 +61,7 @@ struct Prob {
   int gs;               // 1: stored-Gram layout (small_gs.cuh), 0: Gram recomputed in the gradient
   int pad;              // gs: pair rows padded so both gradient orientations are bank-conflict free
   int np;               // gs: physical pair slots (padded rows + one zero slot)
+  int dual;             // gs anneal: room for a second set of normalised columns (fused central difference, hvp_cta_gs)
 };
 
 // Stored-Gram layout (small_gs.cuh): pair (a, b), a < b, lives in slot
@@ -93,6 +94,7 @@ __host__ __device__ inline Prob make_small_prob(bool cplx, int d, int N, int K, 
   P.gs = gs;
   P.pad = gs ? pad : 0;
   P.np = gs ? gs_phys_slots(N, pad) : 0;
+  P.dual = 0;
   return P;
 }
 
@@ -411,6 +413,7 @@ __device__ __forceinline__ bool div_needs_ieee(double a) { return a != 0.0 && fa
 struct Smem {
   double* phiS;      // L*N
   double* alpha;     // N
+  double* alpha2;    // dual: N, norms of the second point (its columns live in phiS, unused by the gs evaluation)
   double* U;         // n (gs: np)
   double* GRI;       // gs: np x C, (Re G, Im G) -> (c Re G, c Im G) per pair slot
   double* phiC;      // gs: N x LP column-major copy of phi (LP = gs_col_stride(L))
@@ -421,6 +424,8 @@ struct Smem {
   double* red;       // 2 * 4 * W
   double* scal;      // 4 scalars (F of the last evaluation, ...)
   int* ired;         // 2 * W
+  // gs Gram sweep, per thread (build_gs_tables): this thread's column k and its rows [gj0, gj1) (gj1 <= k); gk < 0: none
+  int gk, gj0, gj1;
 };
 
 __host__ __device__ inline int mask_words(int N) { return (N + 31) / 32; }

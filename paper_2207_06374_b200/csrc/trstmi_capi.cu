@@ -324,6 +324,13 @@ int trstmi_random_frames(int field, int64_t d, int64_t N, uint64_t seed, int64_t
   return TRSTMI_OK;
 }
 
+int trstmi_random_frame_seeded(int field, int64_t d, int64_t N, uint64_t rng_seed, double* frame) {
+  if (d < 1 || N < 1 || !frame) return TRSTMI_ERR_INVALID_ARG;
+  trstmi_host::SplitMix64 rng(rng_seed);
+  trstmi_host::random_frame(field == TRSTMI_COMPLEX, d, N, rng, frame);
+  return TRSTMI_OK;
+}
+
 int trstmi_ctx_create(int device, trstmi_ctx** out) {
   *out = nullptr;
   int n = 0;
@@ -668,12 +675,29 @@ static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cu
   const int S = trstmi_lanes(c->field, c->d, c->N);
   const KernelSet* ks = find_kernels(c->field == TRSTMI_COMPLEX, c->d, S, A.P.gs);
   if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
-  const size_t bytes = (size_t)anneal_smem_doubles(A.P, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
+  A.P.dual = 0;
+  size_t bytes = (size_t)anneal_smem_doubles(A.P, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "trial state exceeds one SM's shared memory");
   CUDA_TRY(ctx, cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   int per_sm = 0;
   CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks->anneal, S, bytes));
   if (per_sm < 1) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "anneal kernel cannot be resident");
+  if (A.P.gs && A.P.dim <= kGsDualElems * S) {
+    // dual layout (both points of a central difference normalised side by side, hvp_cta_gs): taken when its extra
+    // shared memory costs no resident trial; results are bit-identical either way
+    Prob Pd = A.P;
+    Pd.dual = 1;
+    const size_t bytes_d = (size_t)anneal_smem_doubles(Pd, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
+    int per_sm_d = 0;
+    if (bytes_d <= 227 * 1024 &&
+        cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_d) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, ks->anneal, S, bytes_d) == cudaSuccess &&
+        per_sm_d >= per_sm && !std::getenv("TRSTMI_NO_DUAL")) {
+      A.P.dual = 1;
+      bytes = bytes_d;
+    }
+    (void)cudaGetLastError();
+  }
   const long long grid = std::min<long long>(A.n_list, (long long)per_sm * ctx->sm_count);
   A.counter = ctx->counter;
   CUDA_TRY(ctx, cudaMemsetAsync(ctx->counter, 0, sizeof(int), st));

@@ -2,6 +2,7 @@
 #include "batch_kernels.cuh"
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 using namespace trstmi_dev;
 #ifndef NVEC
@@ -47,5 +48,12 @@ int main(int argc, char** argv) {
   cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
   const double ev = (double)B * 20 / (ms * 1e-3);
   double F0; cudaMemcpy(&F0, F, 8, cudaMemcpyDeviceToHost);
+  std::vector<double> hg(h.size()), hF(B); cudaMemcpy(hg.data(), g, h.size() * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hF.data(), F, B * 8, cudaMemcpyDeviceToHost);
+  unsigned long long hash = 1469598103934665603ULL;  // FNV-1a over the bits of every gradient and F: parity check between variants
+  auto mix = [&](double v) { unsigned long long b; memcpy(&b, &v, 8); hash = (hash ^ b) * 1099511628211ULL; };
+  for (double v : hg) mix(v);
+  for (double v : hF) mix(v);
+  printf("hash %016llx\n", hash);
   printf("gs S=%d K=%d smem %zu (%s / %s): %.4g evals/s, %.0f SM-cycles/eval, F[0]=%.17g\n", SS, P.K, bytes, cudaGetErrorString(e), cudaGetErrorString(e2), ev, 148 * 1.965e9 / ev, F0);
 }

@@ -58,6 +58,7 @@ def lib():
         L.orc_coherence.restype = i64
         L.orc_offdiag_magnitudes.argtypes = [c_int, i64, i64, vp, vp]
         L.orc_distortion_mc.argtypes = [i64, i64, vp, u64, u64, vp, vp]
+        L.orc_altproj_batch.argtypes = [i64, i64, c_int, dbl, dbl, i64, vp, vp, vp, vp, vp]
         L.orc_solve_batch.argtypes = [vp, c_int, i64, vp, vp, vp, vp, vp, vp, c_int]
         L.orc_time_solve_batch.argtypes = [vp, c_int, i64, vp, vp, c_int, vp, vp]
         L.orc_time_solve_batch.restype = dbl
@@ -199,3 +200,16 @@ def distortion_mc(d, N, book, samples, seed):
     est, se = ctypes.c_double(), ctypes.c_double()
     assert lib().orc_distortion_mc(d, N, _p(book), samples, seed, ctypes.byref(est), ctypes.byref(se)) == 0
     return est.value, se.value
+
+
+def altproj_batch(d, N, starts, max_iters=300, mu_target=0.0, tol=1e-10):
+    """alternating_projection (baseline.hpp:68-167) from each start frame: (frames, coherences, iterations, sweeps)."""
+    starts = np.ascontiguousarray(starts, np.float64)
+    R = starts.shape[0]
+    frames = np.empty_like(starts)
+    mu = np.empty(R)
+    it = np.empty(R, np.int32)
+    sw = np.empty(R, np.int32)
+    rc = lib().orc_altproj_batch(d, N, max_iters, mu_target, tol, R, _p(starts), _p(frames), _p(mu), _p(it), _p(sw))
+    assert rc == 0, rc
+    return frames, mu, it, sw

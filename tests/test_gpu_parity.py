@@ -195,6 +195,29 @@ def test_full_budget_trajectories_bit_exact(ctx, field, d, N, trials, max_outer)
     _cmp_solve(g, o, trials, g["n_stages"], 0)
 
 
+@pytest.mark.parametrize("field,d,N,trials,max_outer", [
+    (C, 2, 100, 3, 10),   # config 2 shape: the fused central difference (dual layout) is on by default
+    (C, 6, 36, 3, 20),    # config 3 shape
+    (R, 4, 10, 4, 50),
+])
+def test_fused_central_difference_bit_exact(ctx, field, d, N, trials, max_outer, monkeypatch):
+    """The fused central difference of the anneal kernel (hvp_cta_gs: both points normalised side by side, the +
+    point's combine inside the - point's Gram phase) against the step-by-step path (TRSTMI_NO_DUAL) and the oracle:
+    every record, parameter and frame identical."""
+    from paper_2207_06374_b200 import api
+    cfg = abi.default_cfg(field, d, N, max_outer)
+    cfg.record_cap = 600
+    S = api.lanes(field, d, N)
+    starts, st = api.random_frames(field, d, N, 0, 0, trials)
+    g = ctx.solve_batch(cfg, starts, st)
+    monkeypatch.setenv("TRSTMI_NO_DUAL", "1")
+    g0 = ctx.solve_batch(cfg, starts, st)
+    monkeypatch.delenv("TRSTMI_NO_DUAL")
+    o = orc.solve_batch(cfg, S, starts, st, threads=trials)
+    _cmp_solve(g, o, trials, g["n_stages"], 600)
+    _cmp_solve(g0, o, trials, g0["n_stages"], 600)
+
+
 def test_stage_boundary_rescue(ctx):
     # test_solver.cpp:232-250: column 2 is zero; with a generator the anneal
     # recovers, without one the restart fails with ZeroColumnError(2)
