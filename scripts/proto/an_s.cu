@@ -53,7 +53,11 @@ int main(int argc, char** argv) {
   void* args[] = {&A};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
   cudaEventRecord(e0);
-  cudaLaunchKernel(fn, dim3(T < 148 ? T : 148), dim3(SS), args, bytes, 0);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, SS, bytes);
+  const int grid = T < 148 * per_sm ? T : 148 * per_sm;
+  printf("CTAs per SM %d, grid %d\n", per_sm, grid);
+  cudaLaunchKernel(fn, dim3(grid), dim3(SS), args, bytes, 0);
   cudaEventRecord(e1); cudaError_t e2 = cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
   std::vector<trstmi_trial_out> to(T); cudaMemcpy(to.data(), A.tout, T * sizeof(trstmi_trial_out), cudaMemcpyDeviceToHost);
   std::vector<double> fr(h.size()); cudaMemcpy(fr.data(), A.frames, h.size() * 8, cudaMemcpyDeviceToHost);
