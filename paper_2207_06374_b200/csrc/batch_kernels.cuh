@@ -82,8 +82,14 @@ __global__ void __launch_bounds__(S, (S >= 512 ? 1 : 512 / S)) hvp_batch_kernel(
       path = TRSTMI_HVP_ZERO_DIR;
     } else {
       const double h = kFdBaseStep * (1.0 + sqrt(nn[1])) / fmax(dn, 1e-300);
-      const int zp = eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, dir, h, delta, sm, rbuf, gp, nullptr, nullptr, nullptr);
-      if (zp < 0) {
+      int zp = INT_MAX - 1;
+      if constexpr (GS) {  // both points in one pass (hvp_cta_gs); a vanishing column falls through to the steps below
+        if (A.P.dual) zp = hvp_cta_gs<CPLX, DMAX, EXACT, S>(A.P, x, dir, h, delta, sm, rbuf, hv);
+      }
+      if (zp == -1) {
+        path = TRSTMI_HVP_CENTRAL;
+      } else if ((zp = eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, dir, h, delta, sm, rbuf, gp, nullptr, nullptr,
+                                                          nullptr)) < 0) {
         const int zm = eval_any<CPLX, DMAX, EXACT, S, GS>(A.P, x, dir, -h, delta, sm, rbuf, gm, nullptr, nullptr, nullptr);
         if (zm < 0) {
           const double h2 = 2.0 * h;

@@ -325,13 +325,33 @@ __device__ __forceinline__ GsZ gs_exp_z(const Prob& P, const Smem& sm, double s,
     // triples the sweep's code and slowed every phase by 15 % (profiles/r2_c2_occupancy_experiments.md)
     exp_sweep(std::integral_constant<int, (S <= 64 ? 2 : 5)>{});
   }
-  double zz[3] = {zl, (double)nnz, (double)tiny};
-  block_sum<S, 3>(zz, sm.red, rbuf);
+  // one CTA reduction: z by the CAS tree; the two integer flags ride on the same barrier through REDUX (order-free)
+  int flags = __reduce_add_sync(FULL, nnz) | (__reduce_or_sync(FULL, (unsigned)(tiny != 0)) ? (1 << 24) : 0);
+  {
+    constexpr int W = S / 32;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) zl = __dadd_rn(zl, __shfl_xor_sync(FULL, zl, off));
+    if constexpr (W > 1) {
+      double* buf = sm.red + rbuf * (4 * W);
+      int* ibuf = sm.ired + rbuf * W;
+      if ((tid & 31) == 0) {
+        buf[tid >> 5] = zl;
+        ibuf[tid >> 5] = flags;
+      }
+      __syncthreads();
+      zl = warp_tree_sum<S>(buf);
+      const int f = (tid & 31) < W ? ibuf[tid & 31] : 0;
+      flags = __reduce_add_sync(FULL, f & 0xffffff) | (__reduce_or_sync(FULL, (unsigned)(f >> 24)) ? (1 << 24) : 0);
+      rbuf ^= 1;
+    } else {
+      __syncwarp();
+    }
+  }
   GsZ r;
-  r.z = zz[0];
-  r.sparse = zz[1] * 4.0 < (double)n;
+  r.z = zl;
+  r.sparse = (long long)(flags & 0xffffff) * 4 < (long long)n;
   r.use_mask = build_mask && r.sparse;
-  r.chkdiv = zz[2] != 0.0;
+  r.chkdiv = (flags >> 24) != 0;
   r.yz = __drcp_rn(r.z);
   return r;
 }

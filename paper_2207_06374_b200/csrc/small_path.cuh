@@ -154,20 +154,28 @@ __device__ __forceinline__ double block_sum1(double v, double* red, int& rbuf) {
 // WS: warps the scratch buffers are strided for (the CAS lane count / 32 when
 // the CTA has fewer threads than CAS lanes, small_rt.cuh) — every reduction
 // of a kernel must use the same stride, or the two alternating buffers overlap.
+// Max of doubles that are never NaN and, when negative, only -inf (the x_p of an evaluation: squared magnitudes, or
+// the -inf a thread without pairs starts from): as signed 64-bit integers they order like the doubles, so the warp
+// maximum is two integer REDUX steps (high words, then the low words of the lanes that hold the highest high word)
+// instead of a five-step shuffle butterfly.  Order-free, hence bit-identical to any fmax tree.
+__device__ __forceinline__ double warp_max_nonneg(double v) {
+  const int hi = __double2hiint(v);
+  const int mh = __reduce_max_sync(FULL, hi);
+  const unsigned lo = hi == mh ? (unsigned)__double2loint(v) : 0u;
+  const unsigned ml = __reduce_max_sync(FULL, lo);
+  return __hiloint2double(mh, (int)ml);
+}
+
 template <int S, int WS = S / 32>
 __device__ __forceinline__ double block_max(double v, double* red, int& rbuf) {
   constexpr int W = S / 32;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+  v = warp_max_nonneg(v);
   if constexpr (W > 1) {
     double* buf = red + rbuf * (4 * WS);
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    v = lane < W ? buf[lane] : buf[0];
-#pragma unroll
-    for (int off = 1; off < W; off <<= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
-    v = __shfl_sync(FULL, v, 0);
+    v = warp_max_nonneg(lane < W ? buf[lane] : buf[0]);
     rbuf ^= 1;
   } else {
     __syncwarp();

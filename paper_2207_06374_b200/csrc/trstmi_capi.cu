@@ -397,6 +397,12 @@ static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t
   const KernelSet* ks = find_kernels(field == TRSTMI_COMPLEX, (int)d, S, A.P.gs);
   if (!ks) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "no kernel family for this shape");
   const void* fn = kind == 0 ? ks->eval : kind == 1 ? ks->hvp : ks->coherence;
+  A.P.dual = 0;
+  if (kind == 1 && A.P.gs && A.P.dim <= kGsDualElems * S && !std::getenv("TRSTMI_NO_DUAL")) {
+    Prob Pd = A.P;  // fused central difference (hvp_cta_gs) where its second set of columns fits
+    Pd.dual = 1;
+    if (smem_doubles(Pd, S, field == TRSTMI_COMPLEX, 3) * (long long)sizeof(double) <= 227 * 1024) A.P.dual = 1;
+  }
   const long long dbl = smem_doubles(A.P, S, field == TRSTMI_COMPLEX, kind == 2 ? 0 : 3);
   const size_t bytes = (size_t)dbl * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "frame too large for the small-frame kernels");
