@@ -54,6 +54,13 @@ def load_library():
     if not os.path.exists(LIB_PATH):
         raise ImportError("libtrstmi_b200.so not built: run __graft_entry__.build() "
                           "(python -m paper_2207_06374_b200.build)")
+    try:
+        # The library links libnccl.so.2; PyTorch bundles a newer NCCL under the same soname and needs ITS symbols.
+        # Whichever loads first serves both, so let torch's copy in first when torch is installed (a later
+        # `import torch` in the same process would otherwise fail with an undefined NCCL symbol).
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     lib = ctypes.CDLL(LIB_PATH)
     c_i64, c_int, c_dbl, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
     lib.trstmi_ctx_create.argtypes = [c_int, ctypes.POINTER(vp)]

@@ -115,27 +115,57 @@ __device__ void cas_dots(const double* const* a, const double* const* b, long lo
         }
       }
     }
+    // The eight groups' 32-lane butterflies (xor 16, 8, 4, 2, 1), transposed: at each of the first three levels a
+    // lane keeps half of the groups it still holds and trades the other half with its partner, so a level costs half
+    // the shuffles of the one before — 9 shuffles per dot for the eight groups instead of 40.  Every sum has the same
+    // two operands as in the plain butterfly (own + partner's value of the same group), hence the same bits.  The
+    // reductions of this kernel are bound by shuffle throughput (one warp-wide SHFL per clock per SM).
+    static_assert(UN == 8, "transposed butterfly is written for eight groups");
 #pragma unroll
-    for (int uu = 0; uu < UN; ++uu)
+    for (int k = 0; k < ND; ++k) {
+      double v[UN];
 #pragma unroll
-      for (int k = 0; k < ND; ++k) {
-        double v = acc[uu][k];
+      for (int uu = 0; uu < UN; ++uu) v[uu] = acc[uu][k];
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
-        if (lane == 0) tot[k * CAS_G + warp + TR_W * (u0 + uu)] = v;
+      for (int half = 4, off = 16; half >= 1; half >>= 1, off >>= 1) {
+        const bool hi = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+          const double send = hi ? v[i] : v[i + half];
+          const double keep = hi ? v[i + half] : v[i];
+          v[i] = __dadd_rn(keep, __shfl_xor_sync(FULL, send, off));
+        }
       }
+      v[0] = __dadd_rn(v[0], __shfl_xor_sync(FULL, v[0], 2));
+      v[0] = __dadd_rn(v[0], __shfl_xor_sync(FULL, v[0], 1));
+      if ((lane & 3) == 0) {
+        const int uu = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+        tot[k * CAS_G + warp + TR_W * (u0 + uu)] = v[0];
+      }
+    }
   }
   __syncthreads();
-  for (int off = 1; off < CAS_G; off <<= 1) {
-    const int per = CAS_G / (2 * off);
-    for (int e = tid; e < ND * per; e += TR_T) {
-      const int k = e / per, i = (e - k * per) * 2 * off;
-      tot[k * CAS_G + i] = __dadd_rn(tot[k * CAS_G + i], tot[k * CAS_G + i + off]);
-    }
-    __syncthreads();
-  }
+  // the 1024 group totals pairwise in index order: levels 1..32 inside each warp's 64 consecutive totals (one add
+  // from memory, then the xor butterfly — the same pairs), the last four levels over the 16 warp values
+  static_assert(CAS_G == 64 * TR_W, "one warp per 64 group totals");
+  __shared__ double wtot[3 * TR_W];
+  static_assert(ND <= 3, "wtot holds three dots");
 #pragma unroll
-  for (int k = 0; k < ND; ++k) out[k] = tot[k * CAS_G];
+  for (int k = 0; k < ND; ++k) {
+    const double2 t2 = *reinterpret_cast<const double2*>(tot + k * CAS_G + 64 * warp + 2 * lane);
+    double v = __dadd_rn(t2.x, t2.y);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+    if (lane == 0) wtot[k * TR_W + warp] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    double v = lane < TR_W ? wtot[k * TR_W + lane] : 0.0;
+#pragma unroll
+    for (int off = 1; off < TR_W; off <<= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, off));
+    out[k] = __shfl_sync(FULL, v, 0);
+  }
   __syncthreads();
 }
 
@@ -181,7 +211,7 @@ __device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b 
 __device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }  // std::max
 
 __global__ void __launch_bounds__(TR_T, 1) bde_advance(TrArgs A) {
-  __shared__ double tot[3 * CAS_G];
+  __shared__ __align__(16) double tot[3 * CAS_G];
   __shared__ int sh_int[4];
   const int lane = blockIdx.x;
   const int tid = threadIdx.x;
