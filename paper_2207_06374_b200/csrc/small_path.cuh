@@ -124,23 +124,48 @@ __device__ __forceinline__ double warp_tree_sum(const double* buf) {
 template <int S, int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* red, int& rbuf) {
   constexpr int W = S / 32;
+  if constexpr (K == 2 && W <= 16) {
+    // Two sums at once, transposed (the CTA reductions are bound by shuffle throughput): at the xor-16 level lanes
+    // 0-15 keep the first value and lanes 16-31 the second, each trading the other with its partner, and the four
+    // remaining levels run in both halves at once; the warp totals are combined the same way.  11 shuffles per warp
+    // instead of 20, every add with the operands of the plain butterfly (own + partner's value of the same sum).
+    const int lane = threadIdx.x & 31;
+    const bool hi = (lane & 16) != 0;
+    double t = __dadd_rn(hi ? v[1] : v[0], __shfl_xor_sync(FULL, hi ? v[0] : v[1], 16));
 #pragma unroll
-  for (int k = 0; k < K; ++k)
+    for (int off = 8; off >= 1; off >>= 1) t = __dadd_rn(t, __shfl_xor_sync(FULL, t, off));
+    if constexpr (W > 1) {
+      double* buf = red + rbuf * (4 * W);
+      if ((lane & 15) == 0) buf[(hi ? W : 0) + (threadIdx.x >> 5)] = t;
+      __syncthreads();
+      t = (lane & 15) < W ? buf[(hi ? W : 0) + (lane & 15)] : 0.0;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) v[k] = __dadd_rn(v[k], __shfl_xor_sync(FULL, v[k], off));
-  if constexpr (W > 1) {
-    double* buf = red + rbuf * (4 * W);
-    const int warp = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) buf[k * W + warp] = v[k];
+      for (int off = 1; off < W; off <<= 1) t = __dadd_rn(t, __shfl_xor_sync(FULL, t, off));
+      rbuf ^= 1;
+    } else {
+      __syncwarp();
     }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = warp_tree_sum<S>(buf + k * W);
-    rbuf ^= 1;
+    v[0] = __shfl_sync(FULL, t, 0);
+    v[1] = __shfl_sync(FULL, t, 16);
   } else {
-    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) v[k] = __dadd_rn(v[k], __shfl_xor_sync(FULL, v[k], off));
+    if constexpr (W > 1) {
+      double* buf = red + rbuf * (4 * W);
+      const int warp = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) buf[k * W + warp] = v[k];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k] = warp_tree_sum<S>(buf + k * W);
+      rbuf ^= 1;
+    } else {
+      __syncwarp();
+    }
   }
 }
 
