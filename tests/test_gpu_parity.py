@@ -218,6 +218,30 @@ def test_fused_central_difference_bit_exact(ctx, field, d, N, trials, max_outer,
     _cmp_solve(g0, o, trials, g0["n_stages"], 600)
 
 
+@pytest.mark.parametrize("field,d,N", [(C, 3, 100), (C, 2, 80), (C, 3, 44), (C, 2, 65), (C, 1, 35), (R, 4, 40),
+                                       (C, 2, 110), (C, 8, 12), (R, 3, 7)])
+def test_fused_central_difference_every_layout(ctx, field, d, N, monkeypatch):
+    """The fused central difference against the step-by-step path on one shape per stored-Gram kernel family and CAS
+    width (and on shapes where the dual layout is not taken): identical records, parameters and frames."""
+    from paper_2207_06374_b200 import api
+    cfg = abi.default_cfg(field, d, N, 6)
+    cfg.record_cap = 100
+    starts, st = api.random_frames(field, d, N, 3, 0, 3)
+    g = ctx.solve_batch(cfg, starts, st)
+    monkeypatch.setenv("TRSTMI_NO_DUAL", "1")
+    g0 = ctx.solve_batch(cfg, starts, st)
+    monkeypatch.delenv("TRSTMI_NO_DUAL")
+    _cmp_solve(g, g0, 3, g["n_stages"], 100)
+    # and the single-point HVP entry, which takes the same fused path
+    pts = frames_for(field, d, N, [31, 32])
+    dirs = frames_for(field, d, N, [41, 42])
+    hv, path, zc = ctx.hvp_batch(field, d, N, pts, dirs, 1e-2)
+    monkeypatch.setenv("TRSTMI_NO_DUAL", "1")
+    hv0, path0, zc0 = ctx.hvp_batch(field, d, N, pts, dirs, 1e-2)
+    monkeypatch.delenv("TRSTMI_NO_DUAL")
+    assert np.array_equal(bits(hv), bits(hv0)) and np.array_equal(path, path0) and np.array_equal(zc, zc0)
+
+
 def test_stage_boundary_rescue(ctx):
     # test_solver.cpp:232-250: column 2 is zero; with a generator the anneal
     # recovers, without one the restart fails with ZeroColumnError(2)
