@@ -270,6 +270,15 @@ int trstmi_best_of_ranks(trstmi_ctx* ctx, int64_t dim, double local_mu, int64_t 
 int trstmi_solve_sharded(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restarts, uint64_t seed, double* best_frame,
                          double* best_coherence, int64_t* best_restart, trstmi_trial_out* local_trial_out,
                          int64_t* local_first, int64_t* local_count);
+/* solve() over several GPUs of one process (the reference's restart pool with
+ * one worker per GPU, solver.hpp:239-254): one host thread and one context per
+ * entry of `devices` (a device may repeat), restart blocks by
+ * trstmi_shard_range, best-of on the host in restart order (strict <), no NCCL.
+ * The result equals trstmi_solve's bit for bit for any device list.  trial_out
+ * (restarts entries) / stage_out (restarts x stages) nullable. */
+int trstmi_solve_devices(const int* devices, int ndev, const trstmi_cfg* cfg, int64_t restarts, uint64_t seed,
+                         double* best_frame, double* best_coherence, int64_t* best_restart,
+                         trstmi_trial_out* trial_out, trstmi_stage_out* stage_out);
 
 /* Child seed of restart `index` (mix_seed, rng.hpp:13-18): RestartRecord::seed. */
 uint64_t trstmi_mix_seed(uint64_t seed, uint64_t index);

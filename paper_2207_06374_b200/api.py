@@ -97,6 +97,7 @@ def load_library():
     lib.trstmi_solve_sharded.argtypes = [vp, vp, c_i64, ctypes.c_uint64, vp, vp, vp, vp, vp, vp]
     lib.trstmi_random_frame_seeded.argtypes = [c_int, c_i64, c_i64, ctypes.c_uint64, vp]
     lib.trstmi_altproj_batch.argtypes = [c_i64, c_i64, ctypes.c_int32, c_dbl, c_dbl, c_i64, vp, vp, vp, vp, vp]
+    lib.trstmi_solve_devices.argtypes = [vp, c_int, vp, c_i64, ctypes.c_uint64, vp, vp, vp, vp, vp]
     lib.trstmi_launch_count.restype = ctypes.c_longlong
     lib.trstmi_measure_dfma_peak.argtypes = [vp, c_int, vp]
     _lib = lib
@@ -261,6 +262,28 @@ def random_frames(field, d, N, seed, first, count):
     if rc:
         raise ValueError("random_frame: need d, N >= 1")
     return f, st
+
+
+def solve_devices(cfg, restarts, seed, devices):
+    """solve() (solver.hpp:210-273) over the listed GPUs of this process: one host thread and one context per entry
+    (trstmi_solve_devices).  Returns (best_frame, best_coherence, best_restart, trial_out, stage_out)."""
+    lib = load_library()
+    dim = abi.dim_of(cfg.field, cfg.d, cfg.N)
+    ns = cfg.n_stages or len(default_schedule(cfg.N, cfg.eps_target))
+    devs = (ctypes.c_int * len(devices))(*devices)
+    best = np.empty(dim)
+    mu = ctypes.c_double()
+    idx = ctypes.c_int64()
+    to = (abi.TrialOut * max(restarts, 1))()
+    so = (abi.StageOut * max(restarts * ns, 1))()
+    rc = lib.trstmi_solve_devices(ctypes.cast(devs, ctypes.c_void_p), len(devices), ctypes.byref(cfg), restarts,
+                                  ctypes.c_uint64(seed), _p(best), ctypes.byref(mu), ctypes.byref(idx),
+                                  ctypes.cast(to, ctypes.c_void_p), ctypes.cast(so, ctypes.c_void_p))
+    if rc == abi.TRSTMI_ERR_NO_DEVICE:
+        raise CudaError("no CUDA device: the TRST-MI B200 path has no CPU fallback")
+    if rc:
+        raise CudaError("trstmi_solve_devices failed with status %d" % rc)
+    return best, mu.value, int(idx.value), to, so
 
 
 # ------------------------------------------------------------------ reference-named API

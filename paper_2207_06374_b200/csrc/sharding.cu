@@ -11,9 +11,11 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/trstmi_b200.h"
@@ -182,6 +184,55 @@ int trstmi_solve_sharded(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restart
   if (rc) return rc;
   SH_CUDA(cudaMemcpyAsync(best_frame, db.p, sizeof(double) * dim, cudaMemcpyDeviceToHost, ctx->stream));
   SH_CUDA(cudaStreamSynchronize(ctx->stream));
+  return TRSTMI_OK;
+}
+
+// solve() (solver.hpp:210-273) over several GPUs of ONE process — the drop-in for a caller that today passes
+// `threads` to solve(): one host thread per listed device (the reference's restart pool, one worker per GPU) anneals
+// the contiguous block trstmi_shard_range gives it on a context of its own; the best-of scan then runs over the
+// blocks in restart order with a strict <, so the result is the single-GPU one bit for bit whatever the device list
+// (a device may be listed more than once).  No NCCL: the exchange is host memory.
+int trstmi_solve_devices(const int* devices, int ndev, const trstmi_cfg* cfg, int64_t restarts, uint64_t seed,
+                         double* best_frame, double* best_coherence, int64_t* best_restart,
+                         trstmi_trial_out* trial_out, trstmi_stage_out* stage_out) {
+  if (!devices || ndev < 1 || !cfg || !best_frame || !best_coherence || !best_restart) return TRSTMI_ERR_INVALID_ARG;
+  if (cfg->d < 1 || cfg->N < 1 || restarts < 1) return TRSTMI_ERR_INVALID_ARG;
+  const int64_t dim = (cfg->field == TRSTMI_COMPLEX ? 2 : 1) * (int64_t)cfg->d * cfg->N;
+  const int n_stages = cfg->n_stages ? cfg->n_stages : trstmi_default_schedule(cfg->N, cfg->eps_target, nullptr, 0);
+  struct Shard {
+    int rc = TRSTMI_OK;
+    int64_t first = 0, count = 0, best = -1;
+    double mu = 0.0;
+    std::vector<double> frame;
+  };
+  std::vector<Shard> sh(ndev);
+  std::vector<std::thread> pool;
+  for (int r = 0; r < ndev; ++r) {
+    trstmi_shard_range(restarts, ndev, r, &sh[r].first, &sh[r].count);
+    sh[r].frame.resize(dim);
+    pool.emplace_back([&, r]() {
+      Shard& S = sh[r];
+      if (S.count == 0) return;
+      trstmi_ctx* c = nullptr;
+      S.rc = trstmi_ctx_create(devices[r], &c);
+      if (S.rc) return;
+      S.rc = trstmi_solve(c, cfg, S.count, seed, S.first, S.frame.data(), &S.mu, &S.best,
+                          trial_out ? trial_out + S.first : nullptr,
+                          stage_out ? stage_out + S.first * std::max(n_stages, 1) : nullptr);
+      trstmi_ctx_destroy(c);
+    });
+  }
+  for (auto& t : pool) t.join();
+  int64_t win = -1;
+  for (int r = 0; r < ndev; ++r) {
+    if (sh[r].count == 0 || sh[r].rc == TRSTMI_ERR_ALL_FAILED) continue;  // a block without a successful restart
+    if (sh[r].rc) return sh[r].rc;
+    if (win < 0 || sh[r].mu < sh[win].mu) win = r;  // strict <: the lowest restart index wins ties (solver.hpp:259)
+  }
+  if (win < 0) return TRSTMI_ERR_ALL_FAILED;
+  *best_coherence = sh[win].mu;
+  *best_restart = sh[win].first + sh[win].best;
+  std::memcpy(best_frame, sh[win].frame.data(), sizeof(double) * dim);
   return TRSTMI_OK;
 }
 

@@ -684,25 +684,29 @@ static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cu
   A.P.dual = 0;
   size_t bytes = (size_t)anneal_smem_doubles(A.P, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "trial state exceeds one SM's shared memory");
-  CUDA_TRY(ctx, cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  // dual layout (both points of a central difference normalised side by side, hvp_cta_gs): taken when its extra
+  // shared memory costs no resident trial; results are bit-identical either way
+  size_t bytes_d = 0;
+  if (A.P.gs && A.P.dim <= kGsDualElems * S && !std::getenv("TRSTMI_NO_DUAL")) {
+    Prob Pd = A.P;
+    Pd.dual = 1;
+    bytes_d = (size_t)anneal_smem_doubles(Pd, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
+    if (bytes_d > 227 * 1024) bytes_d = 0;
+  }
+  // the opt-in is per function and process-wide: only ever ask for the larger of the two sizes, so concurrent
+  // launches from several host threads (trstmi_solve_devices) cannot lower each other's limit
+  CUDA_TRY(ctx, cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max(bytes, bytes_d)));
   int per_sm = 0;
   CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks->anneal, S, bytes));
   if (per_sm < 1) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "anneal kernel cannot be resident");
-  if (A.P.gs && A.P.dim <= kGsDualElems * S) {
-    // dual layout (both points of a central difference normalised side by side, hvp_cta_gs): taken when its extra
-    // shared memory costs no resident trial; results are bit-identical either way
-    Prob Pd = A.P;
-    Pd.dual = 1;
-    const size_t bytes_d = (size_t)anneal_smem_doubles(Pd, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
+  if (bytes_d) {
     int per_sm_d = 0;
-    if (bytes_d <= 227 * 1024 &&
-        cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_d) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, ks->anneal, S, bytes_d) == cudaSuccess &&
-        per_sm_d >= per_sm && !std::getenv("TRSTMI_NO_DUAL")) {
+    CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, ks->anneal, S, bytes_d));
+    if (per_sm_d >= per_sm) {
       A.P.dual = 1;
       bytes = bytes_d;
     }
-    (void)cudaGetLastError();
   }
   const long long grid = std::min<long long>(A.n_list, (long long)per_sm * ctx->sm_count);
   A.counter = ctx->counter;

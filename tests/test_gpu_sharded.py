@@ -55,3 +55,23 @@ def test_best_of_ranks_world1_copies_local(ctx):
                                        ctypes.c_void_p(dst.data_ptr()), ctypes.byref(mu), ctypes.byref(idx), None),
               "best_of_ranks")
     assert mu.value == 0.25 and idx.value == 42 and torch.equal(src, dst)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0, 0]])
+def test_solve_devices_equals_single_gpu_solve(devices):
+    """trstmi_solve_devices (one process, a host thread and a context per listed GPU, restart blocks by
+    trstmi_shard_range, best-of on the host) returns trstmi_solve's result bit for bit for any device list —
+    here the one GPU of the box listed several times, so the blocks anneal concurrently."""
+    import ctypes
+    from paper_2207_06374_b200 import abi, api
+    from paper_2207_06374_b200 import records as rec
+    cfg = abi.default_cfg(abi.COMPLEX, 3, 9, 40)
+    restarts, seed = 11, 20240607
+    ref = rec.solve(cfg, restarts=restarts, seed=seed)
+    best, mu, idx, to, so = api.solve_devices(cfg, restarts, seed, devices)
+    assert mu == ref.best_coherence and idx == ref.best_restart
+    assert np.array_equal(best.view(np.uint64), ref.best_frame.view(np.uint64))
+    for i in range(restarts):
+        assert to[i].status == abi.TRIAL_OK
+        assert to[i].coherence == ref.per_restart[i].coherence
+        assert to[i].stages_done == len(ref.per_restart[i].stages)
