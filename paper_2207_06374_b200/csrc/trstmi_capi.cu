@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -391,6 +392,20 @@ static trstmi_bde_host::Engine* bde_engine(trstmi_ctx* ctx) {
   return ctx->bde;
 }
 
+// Dynamic shared-memory opt-in of a kernel: the attribute is per function and device and shared by every host thread,
+// so it is only ever raised (a launch of a smaller shape from another thread must not lower it under a launch in
+// flight: trstmi_solve_devices, multi-threaded callers).
+static cudaError_t raise_smem_optin(int device, const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> have;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = have[{device, fn}];
+  if (bytes <= cur) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
 // ------------------------------------------------------------------ eval / hvp / coherence
 static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t N, BatchArgs& A, cudaStream_t st) {
   const int S = trstmi_lanes(field, d, N);
@@ -406,7 +421,7 @@ static int batch_launch(trstmi_ctx* ctx, int kind, int field, int64_t d, int64_t
   const long long dbl = smem_doubles(A.P, S, field == TRSTMI_COMPLEX, kind == 2 ? 0 : 3);
   const size_t bytes = (size_t)dbl * sizeof(double);
   if (bytes > 227 * 1024) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "frame too large for the small-frame kernels");
-  CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  CUDA_TRY(ctx, raise_smem_optin(ctx->device, fn, bytes));
   const long long grid = std::min<long long>(A.B, 65535LL);
   if (grid <= 0) return TRSTMI_OK;
   void* args[] = {&A};
@@ -693,10 +708,7 @@ static int launch_anneal(trstmi_ctx* ctx, const trstmi_cfg* c, AnnealArgs& A, cu
     bytes_d = (size_t)anneal_smem_doubles(Pd, S, c->field == TRSTMI_COMPLEX) * sizeof(double);
     if (bytes_d > 227 * 1024) bytes_d = 0;
   }
-  // the opt-in is per function and process-wide: only ever ask for the larger of the two sizes, so concurrent
-  // launches from several host threads (trstmi_solve_devices) cannot lower each other's limit
-  CUDA_TRY(ctx, cudaFuncSetAttribute(ks->anneal, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max(bytes, bytes_d)));
+  CUDA_TRY(ctx, raise_smem_optin(ctx->device, ks->anneal, std::max(bytes, bytes_d)));
   int per_sm = 0;
   CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks->anneal, S, bytes));
   if (per_sm < 1) return fail(ctx, TRSTMI_ERR_UNSUPPORTED, "anneal kernel cannot be resident");
