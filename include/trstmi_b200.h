@@ -272,7 +272,9 @@ int trstmi_solve_sharded(trstmi_ctx* ctx, const trstmi_cfg* cfg, int64_t restart
                          int64_t* local_first, int64_t* local_count);
 /* solve() over several GPUs of one process (the reference's restart pool with
  * one worker per GPU, solver.hpp:239-254): one host thread and one context per
- * entry of `devices` (a device may repeat), restart blocks by
+ * entry of `devices` (a device may repeat for small frames; the large-frame
+ * engine sizes its lanes to the device's free memory, so list each GPU once
+ * there), restart blocks by
  * trstmi_shard_range, best-of on the host in restart order (strict <), no NCCL.
  * The result equals trstmi_solve's bit for bit for any device list.  trial_out
  * (restarts entries) / stage_out (restarts x stages) nullable. */
