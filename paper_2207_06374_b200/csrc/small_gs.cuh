@@ -39,6 +39,14 @@
 namespace trstmi_dev {
 
 constexpr int kGsUnroll = TRSTMI_GS_UNROLL;  // k steps of the branch-free gradient loop in flight
+#ifndef TRSTMI_GS_EXP_WIDE
+#define TRSTMI_GS_EXP_WIDE 5
+#endif
+constexpr int kGsExpWide = TRSTMI_GS_EXP_WIDE;  // pairs per step of the exp sweep (S > 64)
+#ifndef TRSTMI_GS_GRAM_UNROLL
+#define TRSTMI_GS_GRAM_UNROLL 1
+#endif
+constexpr int kGsGramUnroll = TRSTMI_GS_GRAM_UNROLL;  // Gram sweep unroll: 1 measured best in the anneal kernel (registers, code size; profiles/r2_c2_session5.md)
 constexpr int kGsDualElems = 4;              // gradient elements per thread the fused central difference keeps in registers
 
 // Slot tables and zeroed pair arrays.  Once per kernel; ends with a barrier.
@@ -190,7 +198,7 @@ __device__ __forceinline__ double gs_gram_sweep(const Prob& P, const Smem& sm, c
     const int* __restrict__ fk = sm.fk;
     double b[LM];
     load_col<LM, EXACT>(phiC + k * LP, b, C * d);
-#pragma unroll 4
+#pragma unroll kGsGramUnroll
     for (int j = sm.gj0; j < sm.gj1; ++j) {
       double a[LM];
       load_col<LM, EXACT>(phiC + j * LP, a, C * d);
@@ -323,7 +331,7 @@ __device__ __forceinline__ GsZ gs_exp_z(const Prob& P, const Smem& sm, double s,
     // five pairs per step where a thread owns several (config 2: 9.7, config 3: 4.9); the 64-lane layout of
     // tiny frames (a pair or two per thread) keeps two.  One width per kernel: a run-time choice of widths
     // triples the sweep's code and slowed every phase by 15 % (profiles/r2_c2_occupancy_experiments.md)
-    exp_sweep(std::integral_constant<int, (S <= 64 ? 2 : 5)>{});
+    exp_sweep(std::integral_constant<int, (S <= 64 ? 2 : kGsExpWide)>{});
   }
   // one CTA reduction: z by the CAS tree; the two integer flags ride on the same barrier through REDUX (order-free)
   int flags = __reduce_add_sync(FULL, nnz) | (__reduce_or_sync(FULL, (unsigned)(tiny != 0)) ? (1 << 24) : 0);
