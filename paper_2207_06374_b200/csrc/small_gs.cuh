@@ -47,7 +47,10 @@ constexpr int kGsExpWide = TRSTMI_GS_EXP_WIDE;  // pairs per step of the exp swe
 #define TRSTMI_GS_GRAM_UNROLL 1
 #endif
 constexpr int kGsGramUnroll = TRSTMI_GS_GRAM_UNROLL;  // Gram sweep unroll: 1 measured best in the anneal kernel (registers, code size; profiles/r2_c2_session5.md)
-constexpr int kGsDualElems = 4;              // gradient elements per thread the fused central difference keeps in registers
+#ifndef TRSTMI_GS_DUAL_ELEMS
+#define TRSTMI_GS_DUAL_ELEMS 2
+#endif
+constexpr int kGsDualElems = TRSTMI_GS_DUAL_ELEMS;              // gradient elements per thread the fused central difference keeps in registers
 
 // Slot tables and zeroed pair arrays.  Once per kernel; ends with a barrier.
 template <int S, bool CPLX>
